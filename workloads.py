@@ -1,0 +1,41 @@
+"""Seeded synthetic inputs and the BASELINE.json workload table.
+
+A module of its own, shared by the oracle tests, the GPU parity tests and
+bench.py.  It holds none of the method's arithmetic: only the random point
+sets (uniform in [0,1)^3, fp32, n x 3 array-of-structs -- the point clouds of
+the paper's n-body / EDM problem class) and the config
+shapes.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# seeds per BASELINE.json config
+SEED_C2 = 161007394
+SEED_C3 = 161007395
+SEED_C5 = 161007396
+
+#: BASELINE.json configs -> concrete synthetic runs
+CONFIGS = {
+    "C1": dict(m=2, n=1024, rho=16, payload="index_write",
+               desc="m=2, n=1024, block 16x16: lambda2 vs BB packed index write"),
+    "C2": dict(m=2, n=65536, rho=16, payload="edm", seed=SEED_C2,
+               desc="m=2 EDM lower triangle, n=65536 points in d=3 fp32, lambda2 vs BB on 1 B200"),
+    "C3": dict(m=3, n=1024, rho=8, payload="index_write+atm", seed=SEED_C3, eps2=1e-2,
+               desc="m=3, n=1024 tetrahedral index-write plus triple-interaction sum"),
+    "C4": dict(m=2, n=1 << 17, rho=16, payload="index_write",
+               desc="m=2 write-bound packed triangle, n=2^17, volume-sharded"),
+    "C5": dict(m=3, n=2048, rho=8, payload="tc", seed=SEED_C5, R=0.5,
+               desc="m=3 triple correlation over n=2048 random points, lambda3 sharded"),
+}
+
+
+def points(n: int, seed: int) -> np.ndarray:
+    """n x 3 fp32 points, uniform in [0,1)^3, from numpy's PCG64 stream."""
+    return np.random.default_rng(seed).random((n, 3), dtype=np.float32)
+
+
+def clustered_points(n: int, seed: int, copies: int = 4) -> np.ndarray:
+    """Edge-case input: points with exact duplicates (zero distances)."""
+    base = points((n + copies - 1) // copies, seed)
+    return np.ascontiguousarray(np.repeat(base, copies, axis=0)[:n])
