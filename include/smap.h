@@ -1,0 +1,194 @@
+/*
+ * smap.h -- C ABI of the B200-native (sm_100a) recursive simplex thread maps
+ * of arXiv 1610.07394 (Navarro, Bustos, Hitschfeld, "Possibilities of Recursive
+ * GPU Mapping for Discrete Orthogonal Simplices").
+ *
+ * Citations: "P:a-b" = PAPER.md lines a-b; "Ek" = reading k in DESIGN.md s.3.
+ *
+ * What the library computes (DESIGN.md s.1):
+ *   a GPU launch over a compact orthotope of blocks is sent onto a discrete
+ *   orthogonal m-simplex by the O(1) block-space map lambda (m=2: P:346-390;
+ *   m=3: P:565-597, reading R3 = E11/E12), or -- the baseline -- by the
+ *   bounding box f(x) = x plus a filter; every mapped
+ *   element runs one payload of the paper's problem class (P:92-99,
+ *   P:115-117; definitions E15) and the block results are reduced on device.
+ *
+ * Domains (E1, E13, E16) and their packed layouts (position in the nested-loop
+ * enumeration; the kernels use the closed forms):
+ *   m=2 strict     {(i,j): 0 <= j < i < n}         p = i(i-1)/2 + j   V = n(n-1)/2
+ *   m=2 inclusive  {(i,j): 0 <= j <= i < n}        p = i(i+1)/2 + j   V = n(n+1)/2
+ *   m=3 strict     {(i,j,k): 0 <= i < j < k < n}   p = C(k,3) + C(j,2) + i   V = C(n,3)
+ *
+ * Conventions of every entry point:
+ *   - noexcept: errors are returned as smap_status codes, never thrown; the
+ *     message of the last error on the calling thread is smap_last_error().
+ *   - SMAP_E_INVALID is returned before any device work and has no side effect.
+ *   - No CPU fallback exists: without a CUDA device smap_plan returns SMAP_E_CUDA.
+ *   - Ownership: the caller owns `points`, `out` and the stream; a plan owns
+ *     only its own scratch (result block, fp64 partials, staging buffers).
+ *   - A plan may be used from one stream at a time (not re-entrant).
+ */
+#ifndef SMAP_H
+#define SMAP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMAP_ABI_VERSION 1
+
+typedef enum {
+    SMAP_OK = 0,
+    SMAP_E_INVALID = 1,      /* bad arguments: nothing was done */
+    SMAP_E_UNSUPPORTED = 2,  /* valid but not implemented for this combination */
+    SMAP_E_CUDA = 3,         /* CUDA runtime error (message in smap_last_error) */
+    SMAP_E_NOMEM = 4         /* device or pinned allocation failed */
+} smap_status;
+
+typedef enum {
+    SMAP_MAP_BB = 0,         /* bounding box: identity + filter */
+    SMAP_MAP_LAMBDA = 1      /* lambda2 / lambda3 reading R3 */
+} smap_map;
+
+typedef enum {
+    SMAP_DIAG_STRICT = 0,    /* j < i  /  i < j < k */
+    SMAP_DIAG_INCLUSIVE = 1  /* j <= i (the paper's Delta_n^2); m=2 only */
+} smap_diag;
+
+typedef enum {
+    /* one element per thread, rho^m threads per block -- the paper's launch
+     * (P:363-367); blocks at or next to the diagonal are folded (E6, E14).
+     * rho^m <= 1024. */
+    SMAP_GRAN_THREAD = 0,
+    /* one rho^m TILE of elements per 256-thread CTA step: lambda is applied to
+     * tiles (the same map, coarser blocks); threads loop over the tile rows
+     * with lanes on the contiguous axis; diagonal tiles are clipped per row
+     * instead of folded.  m=2: rho in {32,64,128}; m=3: rho in {8,16,32}. */
+    SMAP_GRAN_TILE = 1
+} smap_granularity;
+
+typedef enum {
+    SMAP_PAYLOAD_INDEX_WRITE = 0, /* out[p] = p; uint32 if V <= 2^32 else uint64 */
+    SMAP_PAYLOAD_EDM = 1,         /* m=2 strict: out[p] = ||x_i - x_j||_2, fp32 (E15, E17) */
+    SMAP_PAYLOAD_ATM = 2,         /* m=3: sum of Axilrod-Teller terms (E15), param = eps^2; result stats.sum */
+    SMAP_PAYLOAD_TC = 3,          /* m=3: #{i<j<k: r_ij, r_jk, r_ik < R}, param = R; result stats.tc */
+    SMAP_PAYLOAD_MAP_DUMP = 4,    /* int32[4] per grid block/tile in launch order (see below) */
+    SMAP_PAYLOAD_HITCOUNT = 5,    /* uint32 out[p] += 1 per mapped element (caller zeroes out) */
+    SMAP_PAYLOAD_THREAD_DUMP = 6, /* THREAD gran. only: uint64 per launched thread, p or UINT64_MAX */
+    SMAP_PAYLOAD_EMPTY = 7        /* decode only, no element work (block-scheduling microbenchmark) */
+} smap_payload;
+
+/* smap_run flags */
+#define SMAP_RUN_CHECKSUM     0x1u /* INDEX_WRITE/EDM: accumulate s0, s1 (E21) */
+#define SMAP_RUN_CHECKSUM_MIX 0x2u /* INDEX_WRITE/EDM: also accumulate mix (E21); implies CHECKSUM */
+
+typedef struct smap_plan_s *smap_plan_t;
+
+typedef struct {
+    int     m;            /* 2 or 3 */
+    int64_t n;            /* elements per side; power of two */
+    int     rho;          /* block side (threads per axis for THREAD, elements per axis for TILE); power of two */
+    int     map;          /* smap_map */
+    int     diag;         /* smap_diag */
+    int     granularity;  /* smap_granularity */
+    int     persistent;   /* TILE only: 0 = one CTA per tile; k > 0 = k CTAs per SM looping over tiles */
+    int     shard_rank;   /* 0 .. shard_count-1 */
+    int     shard_count;  /* G: power of two dividing N/2 (lambda only); 1 = unsharded */
+    int     device;       /* CUDA device ordinal; -1 = the calling thread's current device */
+} smap_plan_desc;
+
+typedef struct {
+    /* closed forms of the plan (filled by smap_plan_query and smap_stats_fetch) */
+    uint64_t grid_blocks;      /* blocks (THREAD) or tiles (TILE) of this shard's grid */
+    uint64_t launched_threads; /* grid_blocks * rho^m: launched threads (THREAD) / element slots (TILE) */
+    uint64_t useful_elems;     /* elements of the domain owned by this shard */
+    uint64_t wasted_threads;   /* launched_threads - useful_elems */
+    /* measured by the last smap_run (device results) */
+    uint64_t count;            /* elements the kernel processed */
+    uint64_t s0;               /* sum bits(v)            mod 2^64 (SMAP_RUN_CHECKSUM) */
+    uint64_t s1;               /* sum (p+1) * bits(v)    mod 2^64 (SMAP_RUN_CHECKSUM) */
+    uint64_t mix;              /* sum mix64(p ^ bits(v)*K) mod 2^64 (SMAP_RUN_CHECKSUM_MIX) */
+    double   sum;              /* ATM: sum of terms (fp32 terms, fp32 per-thread, fp64 per CTA, fixed-order finalize) */
+    uint64_t tc;               /* TC: triple count */
+    float    kernel_ms;        /* device time of the last smap_run's kernels (CUDA events on its stream) */
+    uint32_t launches;         /* number of kernels the last smap_run launched */
+} smap_stats;
+
+/* Validate `d`, derive the grid and the closed forms, and allocate the plan's
+ * scratch on d->device.  Host math plus small cudaMalloc's; launches nothing.
+ * SMAP_E_INVALID: m not in {2,3}; n or rho not a power of two; N = n/rho too
+ * small (m=2: N >= 2; m=3 lambda: N >= 8, BB: N >= 1); rho outside the
+ * granularity's range; inclusive with m=3; shard_count not a power of two or
+ * not dividing N/2, or > 1 with BB; persistent with THREAD granularity. */
+smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out);
+
+/* Fill the closed-form fields of *st (others zero).  Host only. */
+smap_status smap_plan_query(smap_plan_t p, smap_stats *st);
+
+/* Bytes `out` must hold for payload pl (0 for reduction-only payloads).
+ * INDEX_WRITE/EDM/HITCOUNT index the FULL packed array of the domain even when
+ * sharded (a shard writes only its own positions): V * sizeof(element).
+ * MAP_DUMP: grid_blocks * 16.  THREAD_DUMP: launched_threads * 8. */
+smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes);
+
+/* Run payload pl over the plan's grid, asynchronously on `stream`
+ * (cudaStream_t; NULL = legacy default stream).
+ *   points: DEVICE pointer to n x 3 fp32 (x,y,z) array-of-structs; required
+ *           for EDM/ATM/TC, ignored otherwise (may be NULL).
+ *   param:  ATM: eps^2 (softening); TC: R (distance threshold); else ignored.
+ *   out:    DEVICE pointer of >= smap_out_bytes bytes, or NULL for ATM/TC/EMPTY.
+ *   flags:  SMAP_RUN_* bits.
+ * The plan's result block is zeroed on the stream first; results are read with
+ * smap_stats_fetch.  SMAP_E_INVALID: payload/m mismatch, missing points/out,
+ * out_bytes too small, THREAD_DUMP with TILE granularity. */
+smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float param,
+                     void *out, size_t out_bytes, uint32_t flags, void *stream);
+
+/* End-to-end variant with a HOST point array: copies host_points (n x 3 fp32;
+ * pinned memory recommended) to the plan's device staging buffer on `stream`,
+ * runs like smap_run, copies the result block back to host and synchronises
+ * the stream; *stats (required) receives the results.  `out` stays a DEVICE
+ * buffer (the packed outputs are consumed on the device). */
+smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, float param,
+                          void *out, size_t out_bytes, uint32_t flags, void *stream,
+                          smap_stats *stats);
+
+/* Synchronise the stream of the last smap_run and copy its results (a few
+ * dozen bytes) into *stats, together with the plan's closed forms. */
+smap_status smap_stats_fetch(smap_plan_t p, smap_stats *stats);
+
+/* Useful-element count V of a domain: C(n,2), n(n+1)/2 or C(n,3).  Host only. */
+uint64_t smap_volume(int m, int64_t n, int diag);
+
+/* Free the plan's scratch.  NULL-safe. */
+void smap_destroy(smap_plan_t p);
+
+/* Message of the last error on the calling thread ("" if none). */
+const char *smap_last_error(void);
+
+int smap_abi_version(void);
+
+/* MAP_DUMP record per grid block (THREAD) or tile (TILE), in launch order:
+ *   int32 {x0, x1, x2, cls}
+ * m=2 lambda: cls 0 off-diagonal block (x0,x1) = (J,I) = lambda2(w);
+ *             cls 1 strict row-0 diagonal pair (x0,x1) = (D1,D2) = (wx, N-1-wx);
+ *             cls 2 inclusive diagonal block x0 = D (row 0: wx, row N: wx + N/2).
+ * m=2 BB:     (x0,x1) = (J,I) = (wx,wy); cls 0 J<I, 3 J==I, 4 J>I (filtered out).
+ * m=3 lambda: (x0,x1,x2) = (I,J,K) sorted block triple; cls 0 inside branch,
+ *             1 reflected branch; cls 2 body-diagonal block x0 = d; cls 3 idle.
+ * m=3 BB:     (I,J,K) = (wx,wy,wz); cls 0 I<J<K, 5 I=J<K, 6 I<J=K, 2 I=J=K, 4 outside.
+ *
+ * Launch order (block-linear id bid; W = N/(2G) columns per shard, wx0 = rank*W):
+ *   lambda2: bid = wy*W + (wx - wx0), wy in [0, N) strict / [0, N] inclusive
+ *   lambda3: bid = (wz*(N/2) + wy)*W + (wx - wx0), wz in [0, 3N/4)
+ *   BB2:     bid = I*N + J;   BB3: bid = (K*N + J)*N + I
+ * Threads (THREAD_DUMP order): t = ty*rho + tx (m=2); t = (c*rho + b)*rho + a (m=3). */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMAP_H */

@@ -75,6 +75,7 @@ _SIGS = {
     "or_cs_array": (i32, [P, i32, u64, u64, P]),
     "or_cs_index": (i32, [i32, i32, u64, u64, u64, i32, P]),
     "or_cs_edm": (i32, [u64, P, u64, u64, i32, P]),
+    "or_map_dump": (i32, [i32, i32, i32, u64, u64, u64, P, u64]),
 }
 
 
@@ -187,6 +188,14 @@ def thread_dump(m, inclusive, bb, n, rho, rank=0, G=1) -> np.ndarray:
     length = grid_blocks(m, inclusive, bb, N, G) * rho ** m
     out = np.empty(length, np.uint64)
     assert lib().or_thread_dump(m, int(inclusive), 0 if bb else 1, n, rho, rank, G, _ptr(out), length) == 0
+    return out
+
+
+def map_dump(m, inclusive, bb, N, rank=0, G=1) -> np.ndarray:
+    """Expected MAP_DUMP records (int32 x 4 per grid block, launch order)."""
+    nb = grid_blocks(m, inclusive, bb, N, G)
+    out = np.empty((nb, 4), np.int32)
+    assert lib().or_map_dump(m, int(inclusive), 0 if bb else 1, N, rank, G, _ptr(out), nb) == 0
     return out
 
 

@@ -792,3 +792,43 @@ int or_cs_edm(uint64_t n, const float *pts, uint64_t lo, uint64_t hi, int nthrea
     cs[0] = c0; cs[1] = c1; cs[2] = c2; cs[3] = c3;
     return 0;
 }
+
+/* ======================================================================
+ * Expected MAP_DUMP records (format of include/smap.h, restated): per grid
+ * block in launch order, int32 {x0, x1, x2, cls}.
+ * ====================================================================== */
+int or_map_dump(int m, int inclusive, int map, uint64_t N, uint64_t rank, uint64_t G, int32_t *out, uint64_t len)
+{
+    uint64_t nb = or_grid_blocks(m, inclusive, map, N, G);
+    if (nb != len) return -1;
+    for (uint64_t bid = 0; bid < nb; bid++) {
+        uint64_t w[3] = {0, 0, 0};
+        or_block_coords(m, inclusive, map, N, rank, G, bid, w);
+        int32_t *r = out + 4 * bid;
+        r[0] = r[1] = r[2] = r[3] = 0;
+        if (m == 2 && map == 0) {
+            r[0] = (int32_t)w[0]; r[1] = (int32_t)w[1];
+            r[3] = w[0] < w[1] ? 0 : (w[0] == w[1] ? 3 : 4);
+        } else if (m == 2) {
+            if (w[1] == 0 && !inclusive) { r[0] = (int32_t)w[0]; r[1] = (int32_t)(N - 1 - w[0]); r[3] = 1; }
+            else if (w[1] == 0) { r[0] = r[1] = (int32_t)w[0]; r[3] = 2; }
+            else if (inclusive && w[1] == N) { r[0] = r[1] = (int32_t)(w[0] + N / 2); r[3] = 2; }
+            else { uint64_t x, y; or_lambda2(w[0], w[1], &x, &y); r[0] = (int32_t)x; r[1] = (int32_t)y; r[3] = 0; }
+        } else if (map == 0) {
+            uint64_t I = w[0], J = w[1], K = w[2];
+            r[0] = (int32_t)I; r[1] = (int32_t)J; r[2] = (int32_t)K;
+            r[3] = (I < J && J < K) ? 0 : (I == J && J < K) ? 5 : (I < J && J == K) ? 6 : (I == J && J == K) ? 2 : 4;
+        } else {
+            int64_t o[6];
+            int c = or_lambda3(N, w[0], w[1], w[2], o);
+            if (c == OR_L3_INSIDE || c == OR_L3_REFLECTED) {
+                r[0] = (int32_t)o[3]; r[1] = (int32_t)o[4]; r[2] = (int32_t)o[5]; r[3] = c;
+            } else if (c == OR_L3_SPARE && o[0] >= 0) {
+                r[0] = r[1] = r[2] = (int32_t)o[0]; r[3] = 2;
+            } else {
+                r[3] = 3;
+            }
+        }
+    }
+    return 0;
+}

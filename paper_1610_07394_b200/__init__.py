@@ -1,0 +1,228 @@
+"""B200-native recursive simplex thread maps (arXiv 1610.07394) -- Python binding.
+
+Thin ctypes marshalling over the C ABI of ``include/smap.h`` (``libsmap.so``,
+built for sm_100a by ``_build.py``).  The functions here carry the C names;
+every step of the hot path runs in the library's CUDA kernels.  PyTorch is
+used only for device memory and streams.  There is no CPU fallback: importing
+this package without the built library raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsmap.so")
+HEADER_PATH = os.path.join(os.path.dirname(_PKG), "include", "smap.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                      " (no CPU fallback exists)")
+_lib = C.CDLL(LIB_PATH)
+
+# ------------------------------------------------------------------ enums
+OK, E_INVALID, E_UNSUPPORTED, E_CUDA, E_NOMEM = range(5)
+MAP = {"bb": 0, "lambda": 1}
+DIAG = {"strict": 0, "inclusive": 1}
+GRAN = {"thread": 0, "tile": 1}
+PAYLOAD = {"index_write": 0, "edm": 1, "atm": 2, "tc": 3, "map_dump": 4, "hitcount": 5,
+           "thread_dump": 6, "empty": 7}
+RUN_CHECKSUM = 0x1
+RUN_CHECKSUM_MIX = 0x2
+
+
+class SmapError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"smap status {status}: {msg}")
+        self.status = status
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [("m", C.c_int), ("n", C.c_int64), ("rho", C.c_int), ("map", C.c_int), ("diag", C.c_int),
+                ("granularity", C.c_int), ("persistent", C.c_int), ("shard_rank", C.c_int),
+                ("shard_count", C.c_int), ("device", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("grid_blocks", C.c_uint64), ("launched_threads", C.c_uint64), ("useful_elems", C.c_uint64),
+                ("wasted_threads", C.c_uint64), ("count", C.c_uint64), ("s0", C.c_uint64), ("s1", C.c_uint64),
+                ("mix", C.c_uint64), ("sum", C.c_double), ("tc", C.c_uint64), ("kernel_ms", C.c_float),
+                ("launches", C.c_uint32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_P = C.c_void_p
+_SIGS = {
+    "smap_plan": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(_P)]),
+    "smap_plan_query": (C.c_int, [_P, C.POINTER(Stats)]),
+    "smap_out_bytes": (C.c_int, [_P, C.c_int, C.POINTER(C.c_size_t)]),
+    "smap_run": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_size_t, C.c_uint32, _P]),
+    "smap_run_host": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_size_t, C.c_uint32, _P, C.POINTER(Stats)]),
+    "smap_stats_fetch": (C.c_int, [_P, C.POINTER(Stats)]),
+    "smap_volume": (C.c_uint64, [C.c_int, C.c_int64, C.c_int]),
+    "smap_destroy": (None, [_P]),
+    "smap_last_error": (C.c_char_p, []),
+    "smap_abi_version": (C.c_int, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype, _fn.argtypes = _res, _args
+
+
+def exported_symbols():
+    """Names of every function declared in include/smap.h (for the ABI test)."""
+    with open(HEADER_PATH) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"\b(smap_[a-z_]+)\s*\(", src)) - {"smap_plan_s"})
+
+
+def smap_last_error() -> str:
+    return _lib.smap_last_error().decode()
+
+
+def _check(status):
+    if status != OK:
+        raise SmapError(status, smap_last_error())
+
+
+def smap_abi_version() -> int:
+    return _lib.smap_abi_version()
+
+
+def smap_volume(m: int, n: int, diag: str = "strict") -> int:
+    return _lib.smap_volume(m, n, DIAG[diag])
+
+
+class Plan:
+    """Owns an smap_plan_t; see smap_plan."""
+
+    def __init__(self, handle, desc: PlanDesc):
+        self.handle = handle
+        self.desc = desc
+
+    @property
+    def m(self): return self.desc.m
+
+    @property
+    def n(self): return self.desc.n
+
+    def __del__(self):
+        smap_destroy(self)
+
+
+def smap_plan(m: int, n: int, rho: int, map: str = "lambda", diag: str = "strict", granularity: str = "thread",
+              persistent: int = 0, shard_rank: int = 0, shard_count: int = 1, device: int = -1) -> Plan:
+    d = PlanDesc(m, n, rho, MAP[map], DIAG[diag], GRAN[granularity], persistent, shard_rank, shard_count, device)
+    h = _P()
+    _check(_lib.smap_plan(C.byref(d), C.byref(h)))
+    return Plan(h, d)
+
+
+def smap_destroy(plan: Plan):
+    if plan is not None and getattr(plan, "handle", None):
+        _lib.smap_destroy(plan.handle)
+        plan.handle = None
+
+
+def smap_plan_query(plan: Plan) -> dict:
+    st = Stats()
+    _check(_lib.smap_plan_query(plan.handle, C.byref(st)))
+    return st.as_dict()
+
+
+def smap_out_bytes(plan: Plan, payload: str) -> int:
+    b = C.c_size_t()
+    _check(_lib.smap_out_bytes(plan.handle, PAYLOAD[payload], C.byref(b)))
+    return b.value
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):                       # numpy (host) array
+        return x.ctypes.data
+    raise TypeError(f"cannot take a pointer of {type(x)}")
+
+
+def _nbytes(x):
+    if x is None:
+        return 0
+    if hasattr(x, "untyped_storage"):
+        return x.numel() * x.element_size()
+    return x.nbytes
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except ImportError:
+            pass
+        return None
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+def smap_run(plan: Plan, payload: str, points=None, param: float = 0.0, out=None, flags: int = 0,
+             stream=None):
+    """Asynchronous launch on `stream` (default: torch's current stream).
+    points/out are DEVICE tensors (or raw device pointers with out_bytes implied)."""
+    _check(_lib.smap_run(plan.handle, PAYLOAD[payload], _ptr(points), float(param), _ptr(out),
+                         _nbytes(out) if not isinstance(out, int) else (1 << 62), flags, _stream(stream)))
+
+
+def smap_run_host(plan: Plan, payload: str, host_points=None, param: float = 0.0, out=None, flags: int = 0,
+                  stream=None) -> dict:
+    """End-to-end call with a HOST point array (copied H2D inside), results
+    copied back to host; synchronous.  `out` stays a device tensor."""
+    st = Stats()
+    _check(_lib.smap_run_host(plan.handle, PAYLOAD[payload], _ptr(host_points), float(param), _ptr(out),
+                              _nbytes(out), flags, _stream(stream), C.byref(st)))
+    return st.as_dict()
+
+
+def smap_stats_fetch(plan: Plan) -> dict:
+    st = Stats()
+    _check(_lib.smap_stats_fetch(plan.handle, C.byref(st)))
+    return st.as_dict()
+
+
+# ------------------------------------------------------------------ torch conveniences
+def out_dtype(plan: Plan, payload: str):
+    import torch
+    if payload == "edm":
+        return torch.float32
+    if payload == "index_write":
+        return torch.int64 if smap_volume(plan.m, plan.n, "inclusive" if plan.desc.diag else "strict") > (1 << 32) \
+            else torch.int32
+    if payload == "hitcount":
+        return torch.int32
+    if payload == "map_dump":
+        return torch.int32
+    if payload == "thread_dump":
+        return torch.int64
+    return None
+
+
+def alloc_out(plan: Plan, payload: str, device="cuda", zero: bool = False):
+    """Device tensor sized by smap_out_bytes (int32/int64 views of uint32/uint64 data)."""
+    import torch
+    nb = smap_out_bytes(plan, payload)
+    if nb == 0:
+        return None
+    dt = out_dtype(plan, payload)
+    cnt = nb // torch.empty((), dtype=dt).element_size()
+    return (torch.zeros if zero else torch.empty)(cnt, dtype=dt, device=device)
+
+
+__all__ = ["smap_plan", "smap_plan_query", "smap_out_bytes", "smap_run", "smap_run_host", "smap_stats_fetch",
+           "smap_volume", "smap_destroy", "smap_last_error", "smap_abi_version", "Plan", "SmapError",
+           "alloc_out", "exported_symbols", "RUN_CHECKSUM", "RUN_CHECKSUM_MIX"]

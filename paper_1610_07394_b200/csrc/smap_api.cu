@@ -1,0 +1,381 @@
+// smap_api.cu -- implementation of the C ABI declared in include/smap.h:
+// argument validation, plan construction (grid extents, shard ranges and the
+// closed forms of DESIGN.md s.5), scratch ownership, kernel dispatch and the
+// deterministic fp64 finalize (a7).  No CPU fallback: every payload runs in
+// the sm_100a kernels of smap_thread{2,3}.cu / smap_tile{2,3}.cu.
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+
+#include "smap.h"
+#include "smap_device.cuh"
+
+using namespace smap;
+
+struct smap_plan_s {
+    smap_plan_desc d;
+    Params P;                 // per-plan launch parameters (pts/out/param set per run)
+    uint64_t V;               // volume of the whole domain
+    uint64_t useful;          // elements owned by this shard
+    uint64_t launched;        // grid_blocks * rho^m
+    int elem64;               // index-write element is uint64
+    int device;
+    unsigned ctas;            // TILE: CTAs launched
+    Result *d_res = nullptr;
+    Result *h_res = nullptr;  // pinned
+    double *d_partials = nullptr;
+    uint64_t npartials = 0;
+    double *d_scratch = nullptr;
+    float *d_stage = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t last_stream = nullptr;
+    uint32_t last_launches = 0;
+    int ran = 0;
+};
+
+static thread_local std::string g_err;
+
+static smap_status fail(smap_status s, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+static smap_status cuda_fail(cudaError_t e, const char *where)
+{
+    return fail(e == cudaErrorMemoryAllocation ? SMAP_E_NOMEM : SMAP_E_CUDA, "%s: %s (%s)", where,
+                cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);       \
+    } while (0)
+
+static bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+static int ilog2(int64_t x) { int l = 0; while ((int64_t)1 << (l + 1) <= x) l++; return l; }
+
+extern "C" {
+
+int smap_abi_version(void) { return SMAP_ABI_VERSION; }
+
+const char *smap_last_error(void) { return g_err.c_str(); }
+
+uint64_t smap_volume(int m, int64_t n, int diag)
+{
+    if (n <= 0) return 0;
+    unsigned __int128 N = (unsigned __int128)n;
+    if (m == 2) return (uint64_t)(diag == SMAP_DIAG_INCLUSIVE ? N * (N + 1) / 2 : N * (N - 1) / 2);
+    if (m == 3) return n < 3 ? 0 : (uint64_t)(N * (N - 1) * (N - 2) / 6);
+    return 0;
+}
+
+smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
+{
+    g_err.clear();
+    if (!d || !out) return fail(SMAP_E_INVALID, "smap_plan: NULL argument");
+    *out = nullptr;
+    const int m = d->m;
+    const int64_t n = d->n;
+    const int rho = d->rho;
+    const bool lam = d->map == SMAP_MAP_LAMBDA;
+    const bool incl = d->diag == SMAP_DIAG_INCLUSIVE;
+    const bool tile = d->granularity == SMAP_GRAN_TILE;
+    const int G = d->shard_count;
+    if (m != 2 && m != 3) return fail(SMAP_E_INVALID, "m must be 2 or 3 (got %d)", m);
+    if (d->map != SMAP_MAP_BB && d->map != SMAP_MAP_LAMBDA) return fail(SMAP_E_INVALID, "bad map %d", d->map);
+    if (d->diag != SMAP_DIAG_STRICT && d->diag != SMAP_DIAG_INCLUSIVE) return fail(SMAP_E_INVALID, "bad diag %d", d->diag);
+    if (d->granularity != SMAP_GRAN_THREAD && d->granularity != SMAP_GRAN_TILE)
+        return fail(SMAP_E_INVALID, "bad granularity %d", d->granularity);
+    if (incl && m != 2) return fail(SMAP_E_INVALID, "inclusive diagonal is m=2 only");
+    if (!is_pow2(n) || n < 2 || n > ((int64_t)1 << 30)) return fail(SMAP_E_INVALID, "n must be a power of two in [2, 2^30] (got %lld)", (long long)n);
+    if (!is_pow2(rho) || rho > n) return fail(SMAP_E_INVALID, "rho must be a power of two <= n (got %d)", rho);
+    if (!tile) {
+        if ((m == 2 && rho > 32) || (m == 3 && rho > 8))
+            return fail(SMAP_E_INVALID, "THREAD granularity needs rho^m <= 1024 (rho=%d, m=%d)", rho, m);
+        if (d->persistent) return fail(SMAP_E_INVALID, "persistent CTAs need TILE granularity");
+    } else {
+        const bool ok = m == 2 ? (rho == 32 || rho == 64 || rho == 128) : (rho == 8 || rho == 16 || rho == 32);
+        if (!ok) return fail(SMAP_E_INVALID, "TILE rho must be in %s (got %d)", m == 2 ? "{32,64,128}" : "{8,16,32}", rho);
+        if (d->persistent < 0) return fail(SMAP_E_INVALID, "persistent must be >= 0");
+    }
+    const int64_t N = n / rho;
+    if (m == 2 && lam && N < 2) return fail(SMAP_E_INVALID, "lambda2 needs N = n/rho >= 2");
+    if (m == 3 && lam && N < 8) return fail(SMAP_E_INVALID, "lambda3 needs N = n/rho >= 8 (body blocks, E14)");
+    if (G < 1 || !is_pow2(G)) return fail(SMAP_E_INVALID, "shard_count must be a power of two >= 1");
+    if (!lam && G != 1) return fail(SMAP_E_INVALID, "BB plans are unsharded");
+    if (lam && (N / 2) % G != 0) return fail(SMAP_E_INVALID, "shard_count %d does not divide N/2 = %lld", G, (long long)(N / 2));
+    if (d->shard_rank < 0 || d->shard_rank >= G) return fail(SMAP_E_INVALID, "shard_rank out of range");
+
+    smap_plan_s *p = new (std::nothrow) smap_plan_s();
+    if (!p) return fail(SMAP_E_NOMEM, "host allocation failed");
+    p->d = *d;
+    Params &P = p->P;
+    memset(&P, 0, sizeof P);
+    P.n = (int)n; P.N = (int)N; P.log2N = ilog2(N); P.rho = rho; P.log2rho = ilog2(rho);
+    if (lam) {
+        P.W = (int)(N / 2 / G); P.log2W = ilog2(P.W); P.wx0 = d->shard_rank * P.W;
+        P.nblocks = m == 2 ? (uint64_t)P.W * (uint64_t)(incl ? N + 1 : N)
+                           : (uint64_t)P.W * (uint64_t)(N / 2) * (uint64_t)(3 * N / 4);
+    } else {
+        P.W = (int)N; P.log2W = P.log2N; P.wx0 = 0;
+        P.nblocks = m == 2 ? (uint64_t)N * N : (uint64_t)N * N * N;
+    }
+    uint64_t rm = 1;
+    for (int k = 0; k < m; k++) rm *= (uint64_t)rho;
+    p->launched = P.nblocks * rm;
+    p->V = smap_volume(m, n, d->diag);
+    p->useful = lam ? p->V / (uint64_t)G : p->V;
+    p->elem64 = p->V > ((uint64_t)1 << 32);
+
+    int dev = d->device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaGetDevice"); }
+    }
+    p->device = dev;
+    cudaError_t e = cudaSetDevice(dev);
+    if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaSetDevice"); }
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaDeviceGetAttribute"); }
+    if (tile) {
+        uint64_t want = d->persistent > 0 ? (uint64_t)d->persistent * (uint64_t)sms : P.nblocks;
+        if (want > P.nblocks) want = P.nblocks;
+        if (want > 0x7fffffffull) { delete p; return fail(SMAP_E_INVALID, "too many tiles for one launch"); }
+        p->ctas = (unsigned)want;
+    } else if (P.nblocks > 0x7fffffffull) {
+        delete p;
+        return fail(SMAP_E_INVALID, "grid of %llu blocks exceeds one launch; use TILE granularity",
+                    (unsigned long long)P.nblocks);
+    }
+    if ((e = cudaMalloc(&p->d_res, sizeof(Result))) != cudaSuccess ||
+        (e = cudaMallocHost(&p->h_res, sizeof(Result))) != cudaSuccess ||
+        (e = cudaEventCreate(&p->ev0)) != cudaSuccess || (e = cudaEventCreate(&p->ev1)) != cudaSuccess) {
+        smap_destroy(p);
+        return cuda_fail(e, "smap_plan scratch");
+    }
+    P.res = p->d_res;
+    *out = p;
+    return SMAP_OK;
+}
+
+smap_status smap_plan_query(smap_plan_t p, smap_stats *st)
+{
+    if (!p || !st) return fail(SMAP_E_INVALID, "smap_plan_query: NULL argument");
+    memset(st, 0, sizeof *st);
+    st->grid_blocks = p->P.nblocks;
+    st->launched_threads = p->launched;
+    st->useful_elems = p->useful;
+    st->wasted_threads = p->launched - p->useful;
+    return SMAP_OK;
+}
+
+static int internal_pl(smap_plan_t p, smap_payload pl)
+{
+    switch (pl) {
+    case SMAP_PAYLOAD_INDEX_WRITE: return p->elem64 ? PL_IW64 : PL_IW32;
+    case SMAP_PAYLOAD_EDM: return PL_EDM;
+    case SMAP_PAYLOAD_ATM: return PL_ATM;
+    case SMAP_PAYLOAD_TC: return PL_TC;
+    case SMAP_PAYLOAD_MAP_DUMP: return PL_MAPD;
+    case SMAP_PAYLOAD_HITCOUNT: return PL_HIT;
+    case SMAP_PAYLOAD_THREAD_DUMP: return PL_TDUMP;
+    case SMAP_PAYLOAD_EMPTY: return PL_EMPTY;
+    }
+    return -1;
+}
+
+smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes)
+{
+    if (!p || !bytes) return fail(SMAP_E_INVALID, "smap_out_bytes: NULL argument");
+    switch (pl) {
+    case SMAP_PAYLOAD_INDEX_WRITE: *bytes = (size_t)p->V * (p->elem64 ? 8 : 4); break;
+    case SMAP_PAYLOAD_EDM: *bytes = (size_t)p->V * 4; break;
+    case SMAP_PAYLOAD_HITCOUNT: *bytes = (size_t)p->V * 4; break;
+    case SMAP_PAYLOAD_MAP_DUMP: *bytes = (size_t)p->P.nblocks * 16; break;
+    case SMAP_PAYLOAD_THREAD_DUMP: *bytes = (size_t)p->launched * 8; break;
+    case SMAP_PAYLOAD_ATM: case SMAP_PAYLOAD_TC: case SMAP_PAYLOAD_EMPTY: *bytes = 0; break;
+    default: return fail(SMAP_E_INVALID, "unknown payload %d", (int)pl);
+    }
+    return SMAP_OK;
+}
+
+smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float param, void *out,
+                     size_t out_bytes, uint32_t flags, void *stream)
+{
+    g_err.clear();
+    if (!p) return fail(SMAP_E_INVALID, "smap_run: NULL plan");
+    const int ipl = internal_pl(p, pl);
+    if (ipl < 0) return fail(SMAP_E_INVALID, "unknown payload %d", (int)pl);
+    const smap_plan_desc &d = p->d;
+    const bool tile = d.granularity == SMAP_GRAN_TILE;
+    const bool lam = d.map == SMAP_MAP_LAMBDA;
+    const bool incl = d.diag == SMAP_DIAG_INCLUSIVE;
+    if (flags & ~(SMAP_RUN_CHECKSUM | SMAP_RUN_CHECKSUM_MIX)) return fail(SMAP_E_INVALID, "unknown flags 0x%x", flags);
+    if (ipl == PL_EDM && (d.m != 2 || incl)) return fail(SMAP_E_INVALID, "EDM is defined on the m=2 strict domain");
+    if ((ipl == PL_ATM || ipl == PL_TC) && d.m != 3) return fail(SMAP_E_INVALID, "ATM/TC are m=3 payloads");
+    if ((ipl == PL_EDM || ipl == PL_ATM || ipl == PL_TC) && !points) return fail(SMAP_E_INVALID, "payload needs points");
+    if (ipl == PL_TDUMP && tile) return fail(SMAP_E_INVALID, "THREAD_DUMP needs THREAD granularity");
+    size_t need = 0;
+    smap_out_bytes(p, pl, &need);
+    if (need > 0 && (!out || out_bytes < need))
+        return fail(SMAP_E_INVALID, "out buffer too small: need %zu bytes, got %zu", need, out ? out_bytes : (size_t)0);
+    const bool csum_pl = ipl == PL_IW32 || ipl == PL_IW64 || ipl == PL_EDM;
+    const int cs = !csum_pl ? 0 : (flags & SMAP_RUN_CHECKSUM_MIX) ? 2 : (flags & SMAP_RUN_CHECKSUM) ? 1 : 0;
+    uint64_t rm = 1;
+    for (int k = 0; k < d.m; k++) rm *= (uint64_t)d.rho;
+    const bool reduces = cs > 0 || ipl == PL_ATM || ipl == PL_TC;
+    if (!tile && reduces && (rm % 32) != 0)
+        return fail(SMAP_E_INVALID, "reductions need rho^m to be a multiple of 32 (rho^m = %llu)", (unsigned long long)rm);
+
+    cudaStream_t s = (cudaStream_t)stream;
+    int cur = -1;
+    CK(cudaGetDevice(&cur));
+    if (cur != p->device) CK(cudaSetDevice(p->device));
+    if (ipl == PL_ATM) {
+        const uint64_t np = tile ? p->ctas : p->P.nblocks;
+        if (np > p->npartials) {
+            cudaFree(p->d_partials); cudaFree(p->d_scratch);
+            p->d_partials = nullptr; p->d_scratch = nullptr; p->npartials = 0;
+            CK(cudaMalloc(&p->d_partials, np * sizeof(double)));
+            CK(cudaMalloc(&p->d_scratch, (finalize_scratch_elems(np) + 1) * sizeof(double)));
+            p->npartials = np;
+        }
+    }
+    Params P = p->P;
+    P.pts = points;
+    P.param = param;
+    P.out = out;
+    P.partials = p->d_partials;
+    uint32_t launches = 0;
+    CK(cudaMemsetAsync(p->d_res, 0, sizeof(Result), s));
+    CK(cudaEventRecord(p->ev0, s));
+    cudaError_t e;
+    if (!tile) e = d.m == 2 ? launch_thread2(P, lam, incl, ipl, cs, s) : launch_thread3(P, lam, ipl, cs, s);
+    else e = d.m == 2 ? launch_tile2(P, d.rho, lam, incl, ipl, cs, p->ctas, s)
+                      : launch_tile3(P, d.rho, lam, ipl, cs, p->ctas, s);
+    if (e == cudaErrorInvalidValue) return fail(SMAP_E_UNSUPPORTED, "no kernel for this plan/payload combination");
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    launches++;
+    if (ipl == PL_ATM) {
+        const uint64_t np = tile ? p->ctas : p->P.nblocks;
+        e = launch_finalize(p->d_partials, np, p->d_scratch, p->d_res, s, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "finalize launch");
+    }
+    CK(cudaEventRecord(p->ev1, s));
+    p->last_stream = s;
+    p->last_launches = launches;
+    p->ran = 1;
+    if (cur != p->device) cudaSetDevice(cur);
+    return SMAP_OK;
+}
+
+static void fill_stats(smap_plan_t p, const Result *r, smap_stats *st)
+{
+    smap_plan_query(p, st);
+    uint64_t v[5] = {0, 0, 0, 0, 0};
+    for (int s = 0; s < kSlots; s++)
+        for (int k = 0; k < 5; k++) v[k] += r->slot[s][k];
+    st->count = v[0]; st->s0 = v[1]; st->s1 = v[2]; st->mix = v[3]; st->tc = v[4];
+    st->sum = r->sum;
+    st->launches = p->last_launches;
+    float ms = 0.f;
+    if (p->ran && cudaEventElapsedTime(&ms, p->ev0, p->ev1) == cudaSuccess) st->kernel_ms = ms;
+}
+
+smap_status smap_stats_fetch(smap_plan_t p, smap_stats *st)
+{
+    if (!p || !st) return fail(SMAP_E_INVALID, "smap_stats_fetch: NULL argument");
+    if (!p->ran) return fail(SMAP_E_INVALID, "smap_stats_fetch before smap_run");
+    CK(cudaEventSynchronize(p->ev1));
+    CK(cudaMemcpy(p->h_res, p->d_res, sizeof(Result), cudaMemcpyDeviceToHost));
+    fill_stats(p, p->h_res, st);
+    return SMAP_OK;
+}
+
+smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, float param, void *out,
+                          size_t out_bytes, uint32_t flags, void *stream, smap_stats *stats)
+{
+    if (!p || !stats) return fail(SMAP_E_INVALID, "smap_run_host: NULL argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const float *dev_pts = nullptr;
+    if (host_points) {
+        const size_t bytes = (size_t)p->P.n * 3 * sizeof(float);
+        if (!p->d_stage) CK(cudaMalloc(&p->d_stage, bytes));
+        CK(cudaMemcpyAsync(p->d_stage, host_points, bytes, cudaMemcpyHostToDevice, s));
+        dev_pts = p->d_stage;
+    }
+    smap_status st = smap_run(p, pl, dev_pts, param, out, out_bytes, flags, stream);
+    if (st != SMAP_OK) return st;
+    CK(cudaMemcpyAsync(p->h_res, p->d_res, sizeof(Result), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fill_stats(p, p->h_res, stats);
+    return SMAP_OK;
+}
+
+void smap_destroy(smap_plan_t p)
+{
+    if (!p) return;
+    if (p->d_res) cudaFree(p->d_res);
+    if (p->h_res) cudaFreeHost(p->h_res);
+    if (p->d_partials) cudaFree(p->d_partials);
+    if (p->d_scratch) cudaFree(p->d_scratch);
+    if (p->d_stage) cudaFree(p->d_stage);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    delete p;
+}
+
+} // extern "C"
+
+// ------------------------------------------------------------------ finalize (a7)
+namespace smap {
+
+constexpr int kFin1Per = 8192;   // partials per first-level CTA
+
+__global__ void __launch_bounds__(256) k_fin1(const double *in, uint64_t n, double *out)
+{
+    const uint64_t base = (uint64_t)blockIdx.x * kFin1Per;
+    double s = 0.0;
+    for (int k = 0; k < kFin1Per / 256; k++) {
+        const uint64_t idx = base + (uint64_t)k * 256 + threadIdx.x;
+        if (idx < n) s += in[idx];
+    }
+    s = block_sum_f64(s);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) k_fin2(const double *in, uint64_t n, Result *res)
+{
+    double s = 0.0;
+    for (uint64_t idx = threadIdx.x; idx < n; idx += 1024) s += in[idx];
+    s = block_sum_f64(s);
+    if (threadIdx.x == 0) res->sum = s;
+}
+
+uint64_t finalize_scratch_elems(uint64_t np) { return (np + kFin1Per - 1) / kFin1Per; }
+
+cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res, cudaStream_t s,
+                            uint32_t *launches)
+{
+    if (np <= 65536) {
+        k_fin2<<<1, 1024, 0, s>>>(partials, np, res);
+        *launches += 1;
+        return cudaGetLastError();
+    }
+    const uint64_t n1 = finalize_scratch_elems(np);
+    k_fin1<<<(unsigned)n1, 256, 0, s>>>(partials, np, scratch);
+    k_fin2<<<1, 1024, 0, s>>>(scratch, n1, res);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+} // namespace smap

@@ -1,0 +1,105 @@
+// smap_thread2.cu -- m = 2, one element per thread, rho x rho threads per block:
+// the paper's launch.  lambda2 decodes the block once (block-
+// uniform), each thread adds its offset; the strict grid's row 0 folds two
+// diagonal blocks (reading E6), the inclusive grid uses rows 0 and N.  The BB
+// baseline launches the N x N box and filters; blocks
+// entirely above the diagonal exit at once.
+#include "smap_device.cuh"
+
+namespace smap {
+
+template <bool LAM, bool INCL, int PL, int CS>
+__global__ void __launch_bounds__(1024) k_thread2(Params P)
+{
+    const uint64_t bid = blockIdx.x;
+    const uint32_t tx = threadIdx.x, ty = threadIdx.y, rho = (uint32_t)P.rho;
+    const Blk2 b = LAM ? decode_lambda2(bid, P, INCL) : decode_bb2(bid, P);
+
+    if (PL == PL_MAPD) {
+        if (tx == 0 && ty == 0)
+            reinterpret_cast<int4 *>(P.out)[bid] = make_int4((int)b.J, (int)b.I, 0, b.cls);
+        return;
+    }
+    if (PL == PL_EMPTY) {                 // decode only (block-scheduling microbenchmark)
+        if (b.I > 0x7fffffffu) P.res->sum = 1.0;   // never true; keeps the decode live
+        return;
+    }
+    const bool need_reduce = CS > 0;
+    if (!LAM && b.cls == 4 && PL != PL_TDUMP) return;   // BB: whole block outside -> exit
+
+    uint32_t i, j;
+    bool valid;
+    if (!LAM) {
+        i = b.I * rho + ty; j = b.J * rho + tx;
+        valid = INCL ? (j <= i) : (j < i);
+    } else if (b.cls == 0) {
+        i = b.I * rho + ty; j = b.J * rho + tx; valid = true;
+    } else if (b.cls == 1) {              // D1 = J keeps tx < ty; D2 = I point-reflected keeps tx > ty
+        if (tx < ty) { i = b.J * rho + ty;           j = b.J * rho + tx; }
+        else         { i = b.I * rho + rho - 1 - ty; j = b.I * rho + rho - 1 - tx; }
+        valid = tx != ty;
+    } else {                              // inclusive diagonal block
+        i = b.J * rho + ty; j = b.J * rho + tx; valid = tx <= ty;
+    }
+    const uint64_t p = INCL ? rank2i(i, j) : rank2s(i, j);
+
+    if (PL == PL_TDUMP) {
+        reinterpret_cast<uint64_t *>(P.out)[bid * rho * rho + ty * rho + tx] = valid ? p : ~0ull;
+        return;
+    }
+    if (!need_reduce && !valid) return;
+
+    Acc<CS> acc;
+    if (valid) {
+        if (PL == PL_IW32) {
+            reinterpret_cast<uint32_t *>(P.out)[p] = (uint32_t)p;
+            acc.add(p, p);
+        } else if (PL == PL_IW64) {
+            reinterpret_cast<uint64_t *>(P.out)[p] = p;
+            acc.add(p, p);
+        } else if (PL == PL_EDM) {
+            const float d = __fsqrt_rn(r2_of(P.pts, j, i));
+            reinterpret_cast<float *>(P.out)[p] = d;
+            acc.add(p, __float_as_uint(d));
+        } else if (PL == PL_HIT) {
+            atomicAdd(reinterpret_cast<unsigned int *>(P.out) + p, 1u);
+        }
+    }
+    if (need_reduce) block_add_slots(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid);
+}
+
+template <bool LAM, bool INCL, int PL, int CS>
+static cudaError_t go2(const Params &P, cudaStream_t s)
+{
+    dim3 block(P.rho, P.rho);
+    k_thread2<LAM, INCL, PL, CS><<<(unsigned)P.nblocks, block, 0, s>>>(P);
+    return cudaGetLastError();
+}
+
+template <bool LAM, bool INCL>
+static cudaError_t pick_pl(const Params &P, int pl, int cs, cudaStream_t s)
+{
+#define CS3(PLV)                                                    \
+    if (pl == PLV) {                                                \
+        if (cs == 0) return go2<LAM, INCL, PLV, 0>(P, s);           \
+        if (cs == 1) return go2<LAM, INCL, PLV, 1>(P, s);           \
+        return go2<LAM, INCL, PLV, 2>(P, s);                        \
+    }
+    CS3(PL_IW32)
+    CS3(PL_IW64)
+    if (!INCL) { CS3(PL_EDM) }
+#undef CS3
+    if (pl == PL_MAPD) return go2<LAM, INCL, PL_MAPD, 0>(P, s);
+    if (pl == PL_HIT) return go2<LAM, INCL, PL_HIT, 0>(P, s);
+    if (pl == PL_TDUMP) return go2<LAM, INCL, PL_TDUMP, 0>(P, s);
+    if (pl == PL_EMPTY) return go2<LAM, INCL, PL_EMPTY, 0>(P, s);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_thread2(const Params &P, bool lam, bool incl, int pl, int cs, cudaStream_t s)
+{
+    if (lam) return incl ? pick_pl<true, true>(P, pl, cs, s) : pick_pl<true, false>(P, pl, cs, s);
+    return incl ? pick_pl<false, true>(P, pl, cs, s) : pick_pl<false, false>(P, pl, cs, s);
+}
+
+} // namespace smap

@@ -1,0 +1,128 @@
+// smap_thread3.cu -- m = 3, one element per thread, rho^3 threads per block
+// (P:565-597 with reading R3).  The block triple is decoded once per block;
+// face blocks (I = J < K) fold the {I=J<K} and {I<J=K} element sets, the
+// spare slab row holds the N body-diagonal blocks (reading E14).  The BB
+// baseline launches the N^3 box and filters i < j < k.
+#include "smap_device.cuh"
+
+namespace smap {
+
+template <bool LAM, int PL, int CS>
+__global__ void __launch_bounds__(512) k_thread3(Params P)
+{
+    const uint64_t bid = blockIdx.x;
+    const uint32_t a = threadIdx.x, bb = threadIdx.y, c = threadIdx.z, rho = (uint32_t)P.rho;
+    const Blk3 B = LAM ? decode_lambda3(bid, P) : decode_bb3(bid, P);
+
+    if (PL == PL_MAPD) {
+        if (a == 0 && bb == 0 && c == 0)
+            reinterpret_cast<int4 *>(P.out)[bid] = make_int4((int)B.I, (int)B.J, (int)B.K, B.cls);
+        return;
+    }
+    if (PL == PL_EMPTY) {
+        if (B.cls != 3 && B.K > 0x7fffffffu) P.res->sum = 1.0;
+        return;
+    }
+    // blocks with no element at all exit as a whole (lambda: idle spare/filler; BB: outside)
+    if (PL != PL_TDUMP && ((LAM && B.cls == 3) || (!LAM && B.cls == 4))) {
+        if (PL == PL_ATM) {               // ATM writes one partial per block
+            if (a == 0 && bb == 0 && c == 0) P.partials[bid] = 0.0;
+        }
+        return;
+    }
+
+    uint32_t i = 0, j = 0, k = 0;
+    bool valid;
+    if (!LAM) {
+        i = B.I * rho + a; j = B.J * rho + bb; k = B.K * rho + c;
+        valid = (B.cls != 4) && i < j && j < k;
+    } else if (B.cls == 3) {
+        valid = false;
+    } else if (B.cls == 2) {              // body block d: a < b < c
+        i = B.I * rho + a; j = B.I * rho + bb; k = B.I * rho + c;
+        valid = a < bb && bb < c;
+    } else if (B.I < B.J) {               // interior block I < J < K
+        i = B.I * rho + a; j = B.J * rho + bb; k = B.K * rho + c;
+        valid = true;
+    } else {                              // face block I = J < K
+        if (a < bb) { i = B.I * rho + a; j = B.I * rho + bb; k = B.K * rho + c; }
+        else        { i = B.I * rho + c; j = B.K * rho + bb; k = B.K * rho + a; }
+        valid = a != bb;
+    }
+    const uint64_t p = valid ? rank3(i, j, k) : 0;
+
+    if (PL == PL_TDUMP) {
+        reinterpret_cast<uint64_t *>(P.out)[(bid * rho + c) * rho * rho + bb * rho + a] = valid ? p : ~0ull;
+        return;
+    }
+
+    if (PL == PL_IW32 || PL == PL_IW64 || PL == PL_HIT) {
+        Acc<CS> acc;
+        if (valid) {
+            if (PL == PL_IW32) { reinterpret_cast<uint32_t *>(P.out)[p] = (uint32_t)p; acc.add(p, p); }
+            if (PL == PL_IW64) { reinterpret_cast<uint64_t *>(P.out)[p] = p; acc.add(p, p); }
+            if (PL == PL_HIT) atomicAdd(reinterpret_cast<unsigned int *>(P.out) + p, 1u);
+        }
+        if (CS > 0) block_add_slots(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid);
+        return;
+    }
+    if (PL == PL_ATM) {
+        double t = 0.0;
+        if (valid) t = (double)atm_term(r2_of(P.pts, i, j), r2_of(P.pts, j, k), r2_of(P.pts, i, k), P.param);
+        const double s = block_sum_f64(t);
+        if (a == 0 && bb == 0 && c == 0) P.partials[bid] = s;
+        const int cnt = __syncthreads_count(valid);
+        if (a == 0 && bb == 0 && c == 0) atomicAdd(&P.res->slot[bid % kSlots][0], (unsigned long long)cnt);
+        return;
+    }
+    if (PL == PL_TC) {
+        bool hit = false;
+        if (valid) {
+            const float R2 = __fmul_rn(P.param, P.param);
+            hit = r2_of(P.pts, i, j) < R2 && r2_of(P.pts, j, k) < R2 && r2_of(P.pts, i, k) < R2;
+        }
+        const int cnt = __syncthreads_count(valid);
+        const int hits = __syncthreads_count(hit);
+        if (a == 0 && bb == 0 && c == 0) {
+            atomicAdd(&P.res->slot[bid % kSlots][0], (unsigned long long)cnt);
+            if (hits) atomicAdd(&P.res->slot[bid % kSlots][4], (unsigned long long)hits);
+        }
+        return;
+    }
+}
+
+template <bool LAM, int PL, int CS>
+static cudaError_t go3(const Params &P, cudaStream_t s)
+{
+    dim3 block(P.rho, P.rho, P.rho);
+    k_thread3<LAM, PL, CS><<<(unsigned)P.nblocks, block, 0, s>>>(P);
+    return cudaGetLastError();
+}
+
+template <bool LAM>
+static cudaError_t pick3(const Params &P, int pl, int cs, cudaStream_t s)
+{
+#define CS3(PLV)                                          \
+    if (pl == PLV) {                                      \
+        if (cs == 0) return go3<LAM, PLV, 0>(P, s);       \
+        if (cs == 1) return go3<LAM, PLV, 1>(P, s);       \
+        return go3<LAM, PLV, 2>(P, s);                    \
+    }
+    CS3(PL_IW32)
+    CS3(PL_IW64)
+#undef CS3
+    if (pl == PL_ATM) return go3<LAM, PL_ATM, 0>(P, s);
+    if (pl == PL_TC) return go3<LAM, PL_TC, 0>(P, s);
+    if (pl == PL_MAPD) return go3<LAM, PL_MAPD, 0>(P, s);
+    if (pl == PL_HIT) return go3<LAM, PL_HIT, 0>(P, s);
+    if (pl == PL_TDUMP) return go3<LAM, PL_TDUMP, 0>(P, s);
+    if (pl == PL_EMPTY) return go3<LAM, PL_EMPTY, 0>(P, s);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_thread3(const Params &P, bool lam, int pl, int cs, cudaStream_t s)
+{
+    return lam ? pick3<true>(P, pl, cs, s) : pick3<false>(P, pl, cs, s);
+}
+
+} // namespace smap

@@ -1,0 +1,102 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configurations that
+bench.py times: sampled outputs the oracle computes one by one, plus the
+order-independent checksums (reading E21) the oracle streams over the whole
+domain on the host cores."""
+import math
+
+import numpy as np
+import pytest
+
+import workloads
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sm():
+    assert torch.cuda.is_available()
+    import paper_1610_07394_b200 as s
+    return s
+
+
+def _sample_pairs(n, k, seed):
+    rng = np.random.default_rng(seed)
+    i = rng.integers(1, n, size=k)
+    j = (rng.random(k) * i).astype(np.int64)
+    # always include the extremes and the diagonal neighbours
+    i = np.concatenate([i, [1, n - 1, n - 1, n // 2]])
+    j = np.concatenate([j, [0, 0, n - 2, n // 2 - 1]])
+    return i, j
+
+
+@pytest.mark.parametrize("cfg", workloads.BENCH_EDM_VARIANTS)
+def test_c2_edm_full(sm, orc, cfg):
+    n = workloads.CONFIGS["C2"]["n"]
+    p = workloads.points(n, workloads.SEED_C2)
+    plan = sm.smap_plan(2, n, **cfg)
+    out = sm.alloc_out(plan, "edm")
+    sm.smap_run(plan, "edm", points=torch.from_numpy(p).cuda(), out=out, flags=sm.RUN_CHECKSUM_MIX)
+    st = sm.smap_stats_fetch(plan)
+    i, j = _sample_pairs(n, 100000, 1)
+    pos = torch.from_numpy(i * (i - 1) // 2 + j).cuda()
+    got = out[pos].cpu().numpy()
+    exp = orc.edm_dist_many(p, i, j)
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+    cs = orc.cs_edm(p)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_c3_index_and_atm_full(sm, orc):
+    c = workloads.CONFIGS["C3"]
+    n = c["n"]
+    p = workloads.points(n, workloads.SEED_C3)
+    for cfg in workloads.BENCH_M3_VARIANTS:
+        plan = sm.smap_plan(3, n, **cfg)
+        out = sm.alloc_out(plan, "index_write")
+        sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM)
+        st = sm.smap_stats_fetch(plan)
+        V = math.comb(n, 3)
+        assert st["count"] == V
+        got = out.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, np.arange(V, dtype=np.uint32))
+        sm.smap_run(plan, "atm", points=torch.from_numpy(p).cuda(), param=c["eps2"])
+        st = sm.smap_stats_fetch(plan)
+        ref = orc.atm_sum(p, np.float32(c["eps2"]))
+        assert abs(st["sum"] - ref) <= 1e-5 * abs(ref)
+
+
+def test_c5_tc_full(sm, orc):
+    c = workloads.CONFIGS["C5"]
+    n = c["n"]
+    p = workloads.points(n, workloads.SEED_C5)
+    ref = orc.tc_count(p, np.float32(c["R"]))
+    for cfg in workloads.BENCH_M3_VARIANTS:
+        plan = sm.smap_plan(3, n, **cfg)
+        sm.smap_run(plan, "tc", points=torch.from_numpy(p).cuda(), param=c["R"])
+        st = sm.smap_stats_fetch(plan)
+        assert st["count"] == math.comb(n, 3)
+        assert st["tc"] == ref
+
+
+def test_c4_index_write_full(sm, orc):
+    n = workloads.CONFIGS["C4"]["n"]
+    V = n * (n - 1) // 2
+    plan = sm.smap_plan(2, n, **workloads.BENCH_C4)
+    out = sm.alloc_out(plan, "index_write")             # 68.7 GB of uint64 on the device
+    assert out.numel() == V and out.dtype == torch.int64
+    sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM_MIX)
+    st = sm.smap_stats_fetch(plan)
+    M = 1 << 64
+    assert st["count"] == V
+    assert st["s0"] == (V * (V - 1) // 2) % M
+    assert st["s1"] == ((V - 1) * V * (V + 1) // 3) % M
+    i, j = _sample_pairs(n, 100000, 2)
+    pos = i * (i - 1) // 2 + j
+    got = out[torch.from_numpy(pos).cuda()].cpu().numpy()
+    assert np.array_equal(got, pos)
+    assert st["mix"] == orc.cs_index(2, False, n)["mix"]
+    del out
+    torch.cuda.empty_cache()

@@ -1,0 +1,260 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle,
+element by element on seeded inputs, at sizes that span several tiles and the
+diagonal/ragged cases, for both maps and both granularities.  Bar: bit-exact
+for coordinates, ranks, indices, counts and fp32 EDM; 1e-5 relative for the
+ATM sum (north_star)."""
+import math
+
+import numpy as np
+import pytest
+
+import workloads
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+MAX64 = np.iinfo(np.uint64).max
+
+
+@pytest.fixture(scope="module")
+def sm():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1610_07394_b200 as s
+    return s
+
+
+def dev_points(p):
+    return torch.from_numpy(np.ascontiguousarray(p)).cuda()
+
+
+def run(sm, plan, payload, points=None, param=0.0, flags=0, zero=False):
+    out = sm.alloc_out(plan, payload, zero=zero)
+    sm.smap_run(plan, payload, points=points, param=param, out=out, flags=flags)
+    st = sm.smap_stats_fetch(plan)
+    return out, st
+
+
+def u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+# ---------------------------------------------------------------- block maps (a2, a3)
+@pytest.mark.parametrize("gran,rho,ns", [("thread", 4, [8, 16, 64, 512, 4096]), ("tile", 32, [64, 256, 2048])])
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+@pytest.mark.parametrize("diag", ["strict", "inclusive"])
+def test_map_dump_m2(sm, orc, gran, rho, ns, map_, diag):
+    for n in ns:
+        plan = sm.smap_plan(2, n, rho, map=map_, diag=diag, granularity=gran)
+        out, _ = run(sm, plan, "map_dump")
+        exp = orc.map_dump(2, diag == "inclusive", map_ == "bb", n // rho)
+        np.testing.assert_array_equal(out.cpu().numpy().reshape(-1, 4), exp)
+
+
+@pytest.mark.parametrize("gran,rho,ns", [("thread", 2, [16, 32, 64, 128, 256, 512]), ("tile", 8, [64, 256, 1024])])
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+def test_map_dump_m3(sm, orc, gran, rho, ns, map_):
+    for n in ns:
+        if map_ == "bb" and (n // rho) > 128:
+            continue
+        plan = sm.smap_plan(3, n, rho, map=map_, granularity=gran)
+        out, _ = run(sm, plan, "map_dump")
+        exp = orc.map_dump(3, False, map_ == "bb", n // rho)
+        np.testing.assert_array_equal(out.cpu().numpy().reshape(-1, 4), exp)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_map_dump_sharded(sm, orc, G):
+    for m, n, rho in [(2, 256, 4), (3, 128, 2)]:
+        for r in range(G):
+            plan = sm.smap_plan(m, n, rho, shard_rank=r, shard_count=G)
+            out, _ = run(sm, plan, "map_dump")
+            exp = orc.map_dump(m, False, False, n // rho, rank=r, G=G)
+            np.testing.assert_array_equal(out.cpu().numpy().reshape(-1, 4), exp)
+
+
+# ---------------------------------------------------------------- thread -> element (a4, a5)
+CASES2 = [(16, 4), (64, 8), (256, 16), (512, 32), (1024, 16)]
+CASES3 = [(16, 2), (64, 4), (64, 8), (128, 8), (256, 8)]
+
+
+@pytest.mark.parametrize("n,rho", CASES2)
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+@pytest.mark.parametrize("diag", ["strict", "inclusive"])
+def test_thread_dump_m2(sm, orc, n, rho, map_, diag):
+    plan = sm.smap_plan(2, n, rho, map=map_, diag=diag)
+    out, _ = run(sm, plan, "thread_dump")
+    np.testing.assert_array_equal(u64(out), orc.thread_dump(2, diag == "inclusive", map_ == "bb", n, rho))
+
+
+@pytest.mark.parametrize("n,rho", CASES3)
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+def test_thread_dump_m3(sm, orc, n, rho, map_):
+    plan = sm.smap_plan(3, n, rho, map=map_)
+    out, _ = run(sm, plan, "thread_dump")
+    np.testing.assert_array_equal(u64(out), orc.thread_dump(3, False, map_ == "bb", n, rho))
+
+
+def _hit_cases():
+    for gran, m, n, rho in [("thread", 2, 1024, 16), ("thread", 2, 64, 4), ("tile", 2, 4096, 128), ("tile", 2, 2048, 64),
+                            ("tile", 2, 64, 32), ("thread", 3, 256, 8), ("thread", 3, 64, 2), ("tile", 3, 256, 32),
+                            ("tile", 3, 256, 16), ("tile", 3, 128, 8)]:
+        for map_ in ("lambda", "bb"):
+            for diag in (("strict", "inclusive") if m == 2 else ("strict",)):
+                yield gran, m, n, rho, map_, diag
+
+
+@pytest.mark.parametrize("gran,m,n,rho,map_,diag", list(_hit_cases()))
+def test_hitcount_exact_cover(sm, gran, m, n, rho, map_, diag):
+    plan = sm.smap_plan(m, n, rho, map=map_, diag=diag, granularity=gran)
+    out, _ = run(sm, plan, "hitcount", zero=True)
+    h = out.cpu().numpy()
+    assert len(h) == sm.smap_volume(m, n, diag)
+    assert (h == 1).all(), f"missing {(h == 0).sum()} duplicated {(h > 1).sum()}"
+
+
+# ---------------------------------------------------------------- payloads (a6) + reductions (a7)
+@pytest.mark.parametrize("gran,rho", [("thread", 16), ("thread", 8), ("tile", 32), ("tile", 64), ("tile", 128)])
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+@pytest.mark.parametrize("diag", ["strict", "inclusive"])
+def test_index_write_m2(sm, orc, gran, rho, map_, diag):
+    n = 2048
+    plan = sm.smap_plan(2, n, rho, map=map_, diag=diag, granularity=gran)
+    out, st = run(sm, plan, "index_write", flags=sm.RUN_CHECKSUM_MIX)
+    exp = orc.index_write(2, diag == "inclusive", n)
+    np.testing.assert_array_equal(u32(out), exp)
+    cs = orc.cs_array(exp)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+
+
+@pytest.mark.parametrize("gran,rho", [("thread", 8), ("thread", 4), ("tile", 8), ("tile", 16), ("tile", 32)])
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+def test_index_write_m3(sm, orc, gran, rho, map_):
+    n = 256
+    plan = sm.smap_plan(3, n, rho, map=map_, granularity=gran)
+    flags = sm.RUN_CHECKSUM_MIX if (gran == "tile" or rho ** 3 % 32 == 0) else 0
+    out, st = run(sm, plan, "index_write", flags=flags)
+    exp = orc.index_write(3, False, n)
+    np.testing.assert_array_equal(u32(out), exp)
+    if flags:
+        cs = orc.cs_array(exp)
+        assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+
+
+@pytest.mark.parametrize("gran,rho", [("thread", 16), ("thread", 32), ("tile", 32), ("tile", 64), ("tile", 128)])
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+@pytest.mark.parametrize("pts", ["uniform", "duplicates"])
+def test_edm_bit_exact(sm, orc, gran, rho, map_, pts):
+    n = 2048
+    p = workloads.points(n, workloads.SEED_C2) if pts == "uniform" else workloads.clustered_points(n, 5)
+    plan = sm.smap_plan(2, n, rho, map=map_, granularity=gran)
+    out, st = run(sm, plan, "edm", points=dev_points(p), flags=sm.RUN_CHECKSUM_MIX)
+    exp = orc.edm(p)
+    got = out.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), \
+        f"{(got.view(np.uint32) != exp.view(np.uint32)).sum()} mismatching elements"
+    cs = orc.cs_array(exp)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+
+
+@pytest.mark.parametrize("gran,rho", [("thread", 8), ("tile", 8), ("tile", 16), ("tile", 32)])
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+@pytest.mark.parametrize("eps2", [1e-2, 0.0])
+def test_atm_sum(sm, orc, gran, rho, map_, eps2):
+    n = 256
+    p = workloads.points(n, workloads.SEED_C3)
+    plan = sm.smap_plan(3, n, rho, map=map_, granularity=gran)
+    _, st = run(sm, plan, "atm", points=dev_points(p), param=eps2)
+    ref = orc.atm_sum(p, np.float32(eps2))
+    assert st["count"] == math.comb(n, 3)
+    assert abs(st["sum"] - ref) <= 1e-5 * abs(ref), (st["sum"], ref)
+
+
+@pytest.mark.parametrize("gran,rho", [("thread", 8), ("tile", 8), ("tile", 16), ("tile", 32)])
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+@pytest.mark.parametrize("R", [0.5, 0.2, 10.0, 0.0])
+def test_tc_count(sm, orc, gran, rho, map_, R):
+    n = 256
+    p = workloads.points(n, workloads.SEED_C5)
+    plan = sm.smap_plan(3, n, rho, map=map_, granularity=gran)
+    _, st = run(sm, plan, "tc", points=dev_points(p), param=R)
+    assert st["count"] == math.comb(n, 3)
+    assert st["tc"] == orc.tc_count(p, np.float32(R))
+
+
+def test_atm_deterministic(sm):
+    n = 512
+    p = dev_points(workloads.points(n, 3))
+    for gran, rho in [("thread", 8), ("tile", 32)]:
+        plan = sm.smap_plan(3, n, rho, granularity=gran)
+        sums = set()
+        for _ in range(3):
+            _, st = run(sm, plan, "atm", points=p, param=1e-2)
+            sums.add(st["sum"])
+        assert len(sums) == 1
+
+
+# ---------------------------------------------------------------- sharding (a8 host logic, emulated on 1 GPU)
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("gran,m,n,rho", [("thread", 2, 1024, 16), ("tile", 2, 4096, 64), ("thread", 3, 256, 8),
+                                          ("tile", 3, 512, 16)])
+def test_shards_partition_exactly(sm, G, gran, m, n, rho):
+    hits = None
+    tot = {"count": 0, "s0": 0, "s1": 0, "mix": 0}
+    for r in range(G):
+        plan = sm.smap_plan(m, n, rho, granularity=gran, shard_rank=r, shard_count=G)
+        out = sm.alloc_out(plan, "hitcount", zero=True) if hits is None else hits
+        sm.smap_run(plan, "hitcount", out=out)
+        hits = out
+        o2, st = run(sm, plan, "index_write", flags=sm.RUN_CHECKSUM_MIX)
+        assert st["count"] == sm.smap_volume(m, n) // G          # exact volume balance (8e)
+        for k in tot:
+            tot[k] = (tot[k] + st[k]) % (1 << 64)
+    assert (hits.cpu().numpy() == 1).all()
+    plan = sm.smap_plan(m, n, rho, granularity=gran)
+    _, st = run(sm, plan, "index_write", flags=sm.RUN_CHECKSUM_MIX)
+    assert all(st[k] == tot[k] for k in tot)
+
+
+# ---------------------------------------------------------------- closed forms vs launch
+@pytest.mark.parametrize("m,n,rho,map_,diag,launched,useful", [
+    (2, 1024, 16, "lambda", "strict", 1024 * 1024 // 2, 1024 * 1023 // 2),
+    (2, 1024, 16, "lambda", "inclusive", 1024 * (1024 + 16) // 2, 1024 * 1025 // 2),
+    (2, 1024, 16, "bb", "strict", 1024 ** 2, 1024 * 1023 // 2),
+    (3, 1024, 8, "lambda", "strict", 3 * 1024 ** 3 // 16, math.comb(1024, 3)),
+    (3, 1024, 8, "bb", "strict", 1024 ** 3, math.comb(1024, 3)),
+])
+def test_plan_closed_forms(sm, m, n, rho, map_, diag, launched, useful):
+    q = sm.smap_plan_query(sm.smap_plan(m, n, rho, map=map_, diag=diag))
+    assert q["launched_threads"] == launched and q["useful_elems"] == useful
+    assert q["wasted_threads"] == launched - useful
+
+
+# ---------------------------------------------------------------- edge cases / errors
+def test_smallest_grids(sm, orc):
+    for m, n, rho in [(2, 2, 1), (2, 8, 4), (3, 8, 1), (3, 16, 2)]:
+        plan = sm.smap_plan(m, n, rho)
+        out, _ = run(sm, plan, "hitcount", zero=True)
+        assert (out.cpu().numpy() == 1).all()
+
+
+def test_invalid_arguments(sm):
+    bad = [dict(m=4, n=64, rho=8), dict(m=2, n=100, rho=4), dict(m=2, n=64, rho=64),
+           dict(m=3, n=32, rho=8), dict(m=3, n=64, rho=8, diag="inclusive"), dict(m=2, n=64, rho=8, shard_count=3),
+           dict(m=2, n=64, rho=8, shard_count=8), dict(m=2, n=64, rho=8, map="bb", shard_count=2),
+           dict(m=2, n=1024, rho=16, granularity="tile"), dict(m=2, n=1024, rho=16, persistent=2)]
+    for kw in bad:
+        with pytest.raises(sm.SmapError) as e:
+            sm.smap_plan(**kw)
+        assert e.value.status == 1, kw
+    plan = sm.smap_plan(2, 256, 16)
+    small = torch.empty(10, dtype=torch.int32, device="cuda")
+    with pytest.raises(sm.SmapError):
+        sm.smap_run(plan, "index_write", out=small)
+    with pytest.raises(sm.SmapError):
+        sm.smap_run(plan, "atm", out=None)        # m=3 payload on an m=2 plan
+    with pytest.raises(sm.SmapError):
+        sm.smap_run(plan, "edm", out=sm.alloc_out(plan, "edm"))   # no points

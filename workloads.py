@@ -30,6 +30,16 @@ CONFIGS = {
 }
 
 
+#: launch configurations bench.py times (parity-tested at full size in
+#: tests/test_gpu_fullsize.py).  Keys are smap_plan keyword arguments.
+BENCH_EDM = dict(rho=128, granularity="tile", persistent=4, map="lambda")
+BENCH_EDM_VARIANTS = [BENCH_EDM, dict(rho=16, granularity="thread", map="lambda"),
+                      dict(rho=128, granularity="tile", persistent=4, map="bb")]
+BENCH_M3 = dict(rho=32, granularity="tile", persistent=4, map="lambda")
+BENCH_M3_VARIANTS = [BENCH_M3, dict(rho=8, granularity="thread", map="lambda")]
+BENCH_C4 = dict(rho=128, granularity="tile", persistent=4, map="lambda")
+
+
 def points(n: int, seed: int) -> np.ndarray:
     """n x 3 fp32 points, uniform in [0,1)^3, from numpy's PCG64 stream."""
     return np.random.default_rng(seed).random((n, 3), dtype=np.float32)
