@@ -1,0 +1,364 @@
+"""bench.py -- the driver's benchmark contract for the recursive simplex maps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N --steps K --warmup W
+
+Workload (BASELINE.json configs[1], the metric's headline config; DESIGN.md s.6):
+    m=2 Euclidean distance matrix, strict lower triangle, n = 65536 points in
+    d=3 fp32 (uniform in [0,1)^3, seed 161007394) -> 2,147,450,880 distances
+    written to the packed layout (8.59 GB).
+One step = one pass of the hot path over the batch: lambda2 tile decode (a2),
+thread->element (a4), packed rank (a5), EDM payload (a6), fused linear
+checksum + count (a7), device result record, and for N > 1 the NCCL
+all-reduce of the record (a8).  Sharding: each rank owns W = N/(2G) columns of
+the lambda2 grid (equal useful volume, DESIGN.md s.7); total work is fixed, so
+scaling is "strong".
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+import workloads
+
+METRIC = "simplex elements/s (λ vs BB speedup) at 1/2/4/8 B200; % HBM/FP32 roofline"
+UNIT = "elements/s"
+N_POINTS = workloads.CONFIGS["C2"]["n"]
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(rows_lo, rows_hi, nthreads=0):
+    """Oracle EDM (fp32 distances + streaming checksum) over rows [lo, hi)."""
+    import oracle
+    p = workloads.points(N_POINTS, workloads.SEED_C2)
+    t0 = time.perf_counter()
+    cs = oracle.cs_edm(p, rows_lo, rows_hi, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return cs, dt
+
+
+def pick_sample_rows(target_pairs):
+    """Contiguous rows ending at n with about `target_pairs` pairs."""
+    n = N_POINTS
+    hi = n
+    lo = hi
+    pairs = 0
+    while lo > 1 and pairs < target_pairs:
+        lo -= 1
+        pairs += lo
+    return lo, hi, pairs
+
+
+def cpu_baseline(target_core_seconds=20.0):
+    import oracle
+    cores = oracle.max_threads()
+    # calibrate on a small sample, then size the sample for ~target_core_seconds of CPU work
+    lo, hi, pairs = pick_sample_rows(2e7)
+    cs, dt = oracle_sample(lo, hi)
+    rate = pairs / max(dt, 1e-6)                                  # pairs per wall second on all cores
+    want = max(2e7, min(rate * target_core_seconds / max(cores, 1), 1.5e9))
+    lo, hi, pairs = pick_sample_rows(want)
+    cs, dt = oracle_sample(lo, hi)
+    return {"value": pairs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"rows {lo}..{hi - 1} of the n={N_POINTS} strict EDM ({pairs} pairs: fp32 distances + "
+                      f"linear/mix checksums, {cores} OpenMP threads, {dt:.2f} s wall)",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import oracle
+    cores = oracle.max_threads()
+    lo, hi, pairs = pick_sample_rows(1.5e8)
+    for _ in range(args.warmup):
+        oracle_sample(lo, hi)
+    times = []
+    for _ in range(args.steps):
+        _, dt = oracle_sample(lo, hi)
+        times.append(dt)
+    tot = sum(times)
+    value = pairs * len(times) / tot
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (uniform [0,1)^3 fp32 points, seed 161007394)",
+        "config": {"workload": "C2: m=2 EDM strict lower triangle, n=65536, d=3 fp32",
+                   "sample_rows": [lo, hi - 1], "pairs_per_step": pairs},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"rows {lo}..{hi - 1} ({pairs} pairs) per step, {cores} OpenMP threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compare", action="store_true", help="skip the lambda-vs-BB side measurements")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1610_07394_b200 as sm
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    G = world
+    assert G == args.gpus or args.gpus == 1 and G == 1, f"--gpus {args.gpus} but WORLD_SIZE={G}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if G > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+
+    n = N_POINTS
+    cfg = dict(workloads.BENCH_EDM)
+    host_pts = torch.from_numpy(workloads.points(n, workloads.SEED_C2)).pin_memory()
+    pts = host_pts.to(dev)
+    plan = sm.smap_plan(2, n, shard_rank=rank, shard_count=G, device=local, **cfg)
+    q = sm.smap_plan_query(plan)
+    V = sm.smap_volume(2, n)
+    out = sm.alloc_out(plan, "edm", device=dev)                 # 8.59 GB, full packed layout
+    rec = torch.zeros(6, dtype=torch.int64, device=dev)
+    flags = sm.RUN_CHECKSUM
+
+    def step():
+        sm.smap_run(plan, "edm", points=pts, out=out, flags=flags, stream=stream)
+        sm.smap_result_reduce(plan, rec, stream=stream)
+        if G > 1:
+            dist.all_reduce(rec[:5])                             # u64 sums: exact mod 2^64
+
+    def barrier():
+        torch.cuda.synchronize()
+        if G > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    # ---- timed region: K steps, events on the launching stream, kernel events per step
+    ke0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ke1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier()
+    t0.record(stream)
+    for k in range(args.steps):
+        ke0[k].record(stream)
+        sm.smap_run(plan, "edm", points=pts, out=out, flags=flags, stream=stream)
+        ke1[k].record(stream)
+        sm.smap_result_reduce(plan, rec, stream=stream)
+        if G > 1:
+            dist.all_reduce(rec[:5])
+    t1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms_local = t0.elapsed_time(t1) / args.steps
+    kern_ms_local = sum(a.elapsed_time(b) for a, b in zip(ke0, ke1)) / args.steps
+    res = sm.result_dict(rec)
+    launches_per_step = sm.smap_stats_fetch(plan)["launches"] + 1
+    tm = torch.tensor([ms_local, kern_ms_local], dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms, kern_ms = float(tm[0]), float(tm[1])
+    value = V / (ms * 1e-3)
+    ok = res["count"] == (V if G > 1 else q["useful_elems"])
+
+    # ---- end to end through the public host-buffer API (H2D points, D2H result every step)
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(2):
+        sm.smap_run_host(plan, "edm", host_points=host_pts, out=out, flags=flags, stream=stream)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    w0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        st = sm.smap_run_host(plan, "edm", host_points=host_pts, out=out, flags=flags, stream=stream)
+        if G > 1:
+            r = torch.tensor([st["count"], st["s0"], st["s1"]], dtype=torch.int64).to(dev)  # noqa: F841
+            dist.all_reduce(r)
+            r.cpu()
+    e1.record(stream)
+    barrier()
+    e2e_ms_local = max(e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3) / e2e_steps
+    te = torch.tensor([e2e_ms_local], dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te[0])
+
+    # ---- lambda vs BB at the same granularity, and at the paper's thread granularity (N = 1 only)
+    compare = None
+    if G == 1 and not args.no_compare:
+        compare = {}
+
+        def time_plan(pl, reps):
+            for _ in range(2):
+                sm.smap_run(pl, "edm", points=pts, out=out, flags=0, stream=stream)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                sm.smap_run(pl, "edm", points=pts, out=out, flags=0, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+
+        for name, c in (("tile", cfg), ("thread_rho16", dict(rho=16, granularity="thread"))):
+            c = {k: v for k, v in c.items() if k != "map"}
+            lam = sm.smap_plan(2, n, map="lambda", **c)
+            bb = sm.smap_plan(2, n, map="bb", **{k: v for k, v in c.items() if k != "order"})
+            reps = 10 if name == "tile" else 4
+            ml, mb = time_plan(lam, reps), time_plan(bb, reps)
+            ql, qb = sm.smap_plan_query(lam), sm.smap_plan_query(bb)
+            compare[name] = {"lambda_ms": round(ml, 4), "bb_ms": round(mb, 4), "speedup": round(mb / ml, 3),
+                             "lambda_launched": ql["launched_threads"], "bb_launched": qb["launched_threads"],
+                             "launch_ratio": round(qb["launched_threads"] / ql["launched_threads"], 4),
+                             "config": c}
+            del lam, bb
+
+    # ---- roofline of the dominant kernel (the EDM kernel)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, copy)" if peak else "fallback (B200_PROFILING.md)"
+    peak = peak or 6650.0
+    alg_bytes = q["useful_elems"] * 4 + n * 12                    # 4 B per pair written + the point set read
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        key = json.dumps({k: cfg[k] for k in sorted(cfg)}, sort_keys=True)
+        traffic = tr.get(key)
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)}
+
+    cpu = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline()
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (uniform [0,1)^3 fp32 points, seed 161007394)",
+            "config": {"workload": "C2: m=2 EDM strict lower triangle, n=65536, d=3 fp32 (BASELINE configs[1])",
+                       "map": "lambda2", "granularity": cfg["granularity"], "tile": cfg["rho"],
+                       "order": cfg.get("order", "rows"), "persistent": cfg.get("persistent", 0),
+                       "elements": V, "parallelism": f"omega_x shards x{G}",
+                       "l2": "output 8.59 GB per step >> 126 MB L2 (no flush needed; points stay L2-resident by design)"},
+            "e2e": {"value": V / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": n * 12,
+                    "d2h_bytes_per_step": 48, "ms_per_step": e2e_ms},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "lambda_vs_bb": compare,
+            "checksum_ok": bool(ok),
+            "result": {k: res[k] for k in ("count", "s0", "s1")},
+        }
+        print(json.dumps(line), flush=True)
+    if G > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -66,7 +66,7 @@ typedef enum {
     /* one rho^m TILE of elements per 256-thread CTA step: lambda is applied to
      * tiles (the same map, coarser blocks); threads loop over the tile rows
      * with lanes on the contiguous axis; diagonal tiles are clipped per row
-     * instead of folded.  m=2: rho in {32,64,128}; m=3: rho in {8,16,32}. */
+     * instead of folded.  m=2: rho in {32,64,128,256}; m=3: rho in {8,16,32}. */
     SMAP_GRAN_TILE = 1
 } smap_granularity;
 
@@ -98,7 +98,13 @@ typedef struct {
     int     shard_rank;   /* 0 .. shard_count-1 */
     int     shard_count;  /* G: power of two dividing N/2 (lambda only); 1 = unsharded */
     int     device;       /* CUDA device ordinal; -1 = the calling thread's current device */
+    int     order;        /* lambda2 launch order (smap_order); ignored otherwise */
 } smap_plan_desc;
+
+typedef enum {
+    SMAP_ORDER_ROWS = 0,    /* block-linear id = wy*W + (wx - wx0) */
+    SMAP_ORDER_SQUARES = 1  /* level by level, one b x b copy square at a time (see the launch-order note) */
+} smap_order;
 
 typedef struct {
     /* closed forms of the plan (filled by smap_plan_query and smap_stats_fetch) */
@@ -149,9 +155,10 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
 
 /* End-to-end variant with a HOST point array: copies host_points (n x 3 fp32;
  * pinned memory recommended) to the plan's device staging buffer on `stream`,
- * runs like smap_run, copies the result block back to host and synchronises
- * the stream; *stats (required) receives the results.  `out` stays a DEVICE
- * buffer (the packed outputs are consumed on the device). */
+ * runs like smap_run, reduces the result on the device (smap_result_reduce),
+ * copies the 48-byte smap_result back to host and synchronises the stream;
+ * *stats (required) receives the results.  `out` stays a DEVICE buffer (the
+ * packed outputs are consumed on the device). */
 smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, float param,
                           void *out, size_t out_bytes, uint32_t flags, void *stream,
                           smap_stats *stats);
@@ -159,6 +166,18 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
 /* Synchronise the stream of the last smap_run and copy its results (a few
  * dozen bytes) into *stats, together with the plan's closed forms. */
 smap_status smap_stats_fetch(smap_plan_t p, smap_stats *stats);
+
+/* Device-side result record of one run (48 bytes). */
+typedef struct {
+    uint64_t count, s0, s1, mix, tc;
+    double   sum;
+} smap_result;
+
+/* Reduce the last smap_run's per-CTA results into one smap_result at the
+ * DEVICE address `dst` (8-byte aligned), asynchronously on `stream` (one small
+ * kernel, no host synchronisation) -- the input of a cross-GPU all-reduce:
+ * the integer fields add exactly mod 2^64 and `sum` adds in fp64. */
+smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream);
 
 /* Useful-element count V of a domain: C(n,2), n(n+1)/2 or C(n,3).  Host only. */
 uint64_t smap_volume(int m, int64_t n, int diag);
@@ -182,7 +201,10 @@ int smap_abi_version(void);
  * m=3 BB:     (I,J,K) = (wx,wy,wz); cls 0 I<J<K, 5 I=J<K, 6 I<J=K, 2 I=J=K, 4 outside.
  *
  * Launch order (block-linear id bid; W = N/(2G) columns per shard, wx0 = rank*W):
- *   lambda2: bid = wy*W + (wx - wx0), wy in [0, N) strict / [0, N] inclusive
+ *   lambda2, SMAP_ORDER_ROWS: bid = wy*W + (wx - wx0), wy in [0, N) strict / [0, N] inclusive
+ *   lambda2, SMAP_ORDER_SQUARES: rows 0 and N as above; for row = bid/W in [b, 2b),
+ *            t = bid - b*W; if b <= W: square s = t / b^2, r = t mod b^2,
+ *            wy = b + r / b, wx = wx0 + s*b + r mod b; else wy = b + t / W, wx = wx0 + t mod W
  *   lambda3: bid = (wz*(N/2) + wy)*W + (wx - wx0), wz in [0, 3N/4)
  *   BB2:     bid = I*N + J;   BB3: bid = (K*N + J)*N + I
  * Threads (THREAD_DUMP order): t = ty*rho + tx (m=2); t = (c*rho + b)*rho + a (m=3). */

@@ -61,8 +61,8 @@ _SIGS = {
     "or_thread_elem2": (i32, [i32, i32, u64, u64, u64, u64, u64, u64, P]),
     "or_thread_elem3": (i32, [i32, u64, u64, u64, u64, u64, u64, u64, u64, P]),
     "or_grid_blocks": (u64, [i32, i32, i32, u64, u64]),
-    "or_thread_dump": (i32, [i32, i32, i32, u64, u64, u64, u64, P, u64]),
-    "or_element_hits": (i32, [i32, i32, i32, u64, u64, u64, u64, P, u64, P]),
+    "or_thread_dump": (i32, [i32, i32, i32, u64, u64, u64, u64, i32, P, u64]),
+    "or_element_hits": (i32, [i32, i32, i32, u64, u64, u64, u64, i32, P, u64, P]),
     "or_column_work": (i64, [i32, i32, u64, u64, u64]),
     "or_index_write": (i32, [i32, i32, u64, P, i32]),
     "or_edm_dist": (f32, [P, u64, u64]),
@@ -75,7 +75,7 @@ _SIGS = {
     "or_cs_array": (i32, [P, i32, u64, u64, P]),
     "or_cs_index": (i32, [i32, i32, u64, u64, u64, i32, P]),
     "or_cs_edm": (i32, [u64, P, u64, u64, i32, P]),
-    "or_map_dump": (i32, [i32, i32, i32, u64, u64, u64, P, u64]),
+    "or_map_dump": (i32, [i32, i32, i32, u64, u64, u64, i32, P, u64]),
 }
 
 
@@ -183,28 +183,32 @@ def grid_blocks(m, inclusive, bb, N, G=1):
     return lib().or_grid_blocks(m, int(inclusive), 0 if bb else 1, N, G)
 
 
-def thread_dump(m, inclusive, bb, n, rho, rank=0, G=1) -> np.ndarray:
+ORDERS = {"rows": 0, "squares": 1}
+
+
+def thread_dump(m, inclusive, bb, n, rho, rank=0, G=1, order="rows") -> np.ndarray:
     N = n // rho
     length = grid_blocks(m, inclusive, bb, N, G) * rho ** m
     out = np.empty(length, np.uint64)
-    assert lib().or_thread_dump(m, int(inclusive), 0 if bb else 1, n, rho, rank, G, _ptr(out), length) == 0
+    assert lib().or_thread_dump(m, int(inclusive), 0 if bb else 1, n, rho, rank, G, ORDERS[order],
+                                _ptr(out), length) == 0
     return out
 
 
-def map_dump(m, inclusive, bb, N, rank=0, G=1) -> np.ndarray:
+def map_dump(m, inclusive, bb, N, rank=0, G=1, order="rows") -> np.ndarray:
     """Expected MAP_DUMP records (int32 x 4 per grid block, launch order)."""
     nb = grid_blocks(m, inclusive, bb, N, G)
     out = np.empty((nb, 4), np.int32)
-    assert lib().or_map_dump(m, int(inclusive), 0 if bb else 1, N, rank, G, _ptr(out), nb) == 0
+    assert lib().or_map_dump(m, int(inclusive), 0 if bb else 1, N, rank, G, ORDERS[order], _ptr(out), nb) == 0
     return out
 
 
-def element_hits(m, inclusive, bb, n, rho, rank=0, G=1, hits=None):
+def element_hits(m, inclusive, bb, n, rho, rank=0, G=1, hits=None, order="rows"):
     V = domain_volume(m, inclusive, n)
     if hits is None:
         hits = np.zeros(V, np.uint32)
     r = np.zeros(3, np.int64)
-    assert lib().or_element_hits(m, int(inclusive), 0 if bb else 1, n, rho, rank, G,
+    assert lib().or_element_hits(m, int(inclusive), 0 if bb else 1, n, rho, rank, G, ORDERS[order],
                                  _ptr(hits), V, _ptr(r)) == 0
     return hits, dict(launched=int(r[0]), useful=int(r[1]), outside=int(r[2]))
 

@@ -465,8 +465,11 @@ uint64_t or_grid_blocks(int m, int inclusive, int map, uint64_t N, uint64_t G)
     return (N / 2 / G) * (N / 2) * (3 * N / 4);
 }
 
+/* The lambda2 "square" launch order (order = 1): rows 0 and N as in row
+ * order; the rows [b, 2b) of level b are enumerated one b x b copy square at
+ * a time (found here by plain search over the levels), row by row. */
 static int or_block_coords(int m, int inclusive, int map, uint64_t N, uint64_t rank, uint64_t G,
-                           uint64_t bid, uint64_t *w)
+                           int order, uint64_t bid, uint64_t *w)
 {
     (void)inclusive;
     if (map == 0) {
@@ -474,6 +477,18 @@ static int or_block_coords(int m, int inclusive, int map, uint64_t N, uint64_t r
         return 0;
     }
     uint64_t W = N / 2 / G, wx0 = rank * W;
+    if (m == 2 && order == 1 && bid / W >= 1 && bid / W < N) {
+        uint64_t b = 1;
+        while (!(bid / W >= b && bid / W < 2 * b)) b *= 2;      /* level containing this row */
+        uint64_t t = bid - b * W;
+        if (b <= W) {
+            uint64_t s = t / (b * b), r = t % (b * b);
+            w[1] = b + r / b; w[0] = wx0 + s * b + r % b;
+        } else {
+            w[1] = b + t / W; w[0] = wx0 + t % W;
+        }
+        return 0;
+    }
     w[0] = wx0 + bid % W; bid /= W;
     if (m == 2) { w[1] = bid; return 0; }
     w[1] = bid % (N / 2); w[2] = bid / (N / 2);
@@ -483,14 +498,14 @@ static int or_block_coords(int m, int inclusive, int map, uint64_t N, uint64_t r
 /* Writes, per launched thread in launch order, the packed rank of its element
  * or UINT64_MAX when idle.  len must equal grid_blocks * rho^m. */
 int or_thread_dump(int m, int inclusive, int map, uint64_t n, uint64_t rho, uint64_t rank,
-                   uint64_t G, uint64_t *out, uint64_t len)
+                   uint64_t G, int order, uint64_t *out, uint64_t len)
 {
     uint64_t N = n / rho, T = or_ipow(rho, m);
     uint64_t nb = or_grid_blocks(m, inclusive, map, N, G);
     if (nb * T != len) return -1;
     for (uint64_t bid = 0; bid < nb; bid++) {
         uint64_t w[3] = {0, 0, 0};
-        or_block_coords(m, inclusive, map, N, rank, G, bid, w);
+        or_block_coords(m, inclusive, map, N, rank, G, order, bid, w);
         for (uint64_t t = 0; t < T; t++) {
             int64_t e[3];
             int ok;
@@ -512,14 +527,14 @@ int or_thread_dump(int m, int inclusive, int map, uint64_t n, uint64_t rho, uint
  * into hits[p] (caller zeroes; length V).  res = {launched, useful, outside}
  * where outside counts elements that are not in the target domain. */
 int or_element_hits(int m, int inclusive, int map, uint64_t n, uint64_t rho, uint64_t rank,
-                    uint64_t G, uint32_t *hits, uint64_t V, int64_t *res)
+                    uint64_t G, int order, uint32_t *hits, uint64_t V, int64_t *res)
 {
     uint64_t N = n / rho, T = or_ipow(rho, m);
     uint64_t nb = or_grid_blocks(m, inclusive, map, N, G);
     int64_t useful = 0, outside = 0;
     for (uint64_t bid = 0; bid < nb; bid++) {
         uint64_t w[3] = {0, 0, 0};
-        or_block_coords(m, inclusive, map, N, rank, G, bid, w);
+        or_block_coords(m, inclusive, map, N, rank, G, order, bid, w);
         for (uint64_t t = 0; t < T; t++) {
             int64_t e[3];
             int ok;
@@ -595,15 +610,17 @@ int or_index_write(int m, int inclusive, uint64_t n, void *out, int elem_bytes)
     return 0;
 }
 
-/* Squared distance in fp32, fixed order ((dx*dx + dy*dy) + dz*dz), d = p_b - p_a. */
+/* Squared distance in fp32 (reading E17): d = p_b - p_a (three rounded
+ * subtractions), r^2 = fma(dz, dz, fma(dy, dy, dx*dx)) with IEEE fused
+ * multiply-adds (C99 fmaf, correctly rounded). */
 static float or_r2(const float *pts, uint64_t a, uint64_t b)
 {
     float dx = pts[3 * b + 0] - pts[3 * a + 0];
     float dy = pts[3 * b + 1] - pts[3 * a + 1];
     float dz = pts[3 * b + 2] - pts[3 * a + 2];
-    float sx = dx * dx, sy = dy * dy, sz = dz * dz;
-    float s = sx + sy;
-    return s + sz;
+    float sx = dx * dx;
+    float sxy = fmaf(dy, dy, sx);
+    return fmaf(dz, dz, sxy);
 }
 
 /* EDM element: Euclidean distance ||x_i - x_j||_2 in fp32,
@@ -797,13 +814,14 @@ int or_cs_edm(uint64_t n, const float *pts, uint64_t lo, uint64_t hi, int nthrea
  * Expected MAP_DUMP records (format of include/smap.h, restated): per grid
  * block in launch order, int32 {x0, x1, x2, cls}.
  * ====================================================================== */
-int or_map_dump(int m, int inclusive, int map, uint64_t N, uint64_t rank, uint64_t G, int32_t *out, uint64_t len)
+int or_map_dump(int m, int inclusive, int map, uint64_t N, uint64_t rank, uint64_t G, int order,
+                int32_t *out, uint64_t len)
 {
     uint64_t nb = or_grid_blocks(m, inclusive, map, N, G);
     if (nb != len) return -1;
     for (uint64_t bid = 0; bid < nb; bid++) {
         uint64_t w[3] = {0, 0, 0};
-        or_block_coords(m, inclusive, map, N, rank, G, bid, w);
+        or_block_coords(m, inclusive, map, N, rank, G, order, bid, w);
         int32_t *r = out + 4 * bid;
         r[0] = r[1] = r[2] = r[3] = 0;
         if (m == 2 && map == 0) {

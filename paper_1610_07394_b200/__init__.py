@@ -26,6 +26,7 @@ OK, E_INVALID, E_UNSUPPORTED, E_CUDA, E_NOMEM = range(5)
 MAP = {"bb": 0, "lambda": 1}
 DIAG = {"strict": 0, "inclusive": 1}
 GRAN = {"thread": 0, "tile": 1}
+ORDER = {"rows": 0, "squares": 1}
 PAYLOAD = {"index_write": 0, "edm": 1, "atm": 2, "tc": 3, "map_dump": 4, "hitcount": 5,
            "thread_dump": 6, "empty": 7}
 RUN_CHECKSUM = 0x1
@@ -41,7 +42,7 @@ class SmapError(RuntimeError):
 class PlanDesc(C.Structure):
     _fields_ = [("m", C.c_int), ("n", C.c_int64), ("rho", C.c_int), ("map", C.c_int), ("diag", C.c_int),
                 ("granularity", C.c_int), ("persistent", C.c_int), ("shard_rank", C.c_int),
-                ("shard_count", C.c_int), ("device", C.c_int)]
+                ("shard_count", C.c_int), ("device", C.c_int), ("order", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -62,6 +63,7 @@ _SIGS = {
     "smap_run": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_size_t, C.c_uint32, _P]),
     "smap_run_host": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_size_t, C.c_uint32, _P, C.POINTER(Stats)]),
     "smap_stats_fetch": (C.c_int, [_P, C.POINTER(Stats)]),
+    "smap_result_reduce": (C.c_int, [_P, _P, _P]),
     "smap_volume": (C.c_uint64, [C.c_int, C.c_int64, C.c_int]),
     "smap_destroy": (None, [_P]),
     "smap_last_error": (C.c_char_p, []),
@@ -114,8 +116,10 @@ class Plan:
 
 
 def smap_plan(m: int, n: int, rho: int, map: str = "lambda", diag: str = "strict", granularity: str = "thread",
-              persistent: int = 0, shard_rank: int = 0, shard_count: int = 1, device: int = -1) -> Plan:
-    d = PlanDesc(m, n, rho, MAP[map], DIAG[diag], GRAN[granularity], persistent, shard_rank, shard_count, device)
+              persistent: int = 0, shard_rank: int = 0, shard_count: int = 1, device: int = -1,
+              order: str = "rows") -> Plan:
+    d = PlanDesc(m, n, rho, MAP[map], DIAG[diag], GRAN[granularity], persistent, shard_rank, shard_count, device,
+                 ORDER[order])
     h = _P()
     _check(_lib.smap_plan(C.byref(d), C.byref(h)))
     return Plan(h, d)
@@ -193,6 +197,26 @@ def smap_stats_fetch(plan: Plan) -> dict:
     st = Stats()
     _check(_lib.smap_stats_fetch(plan.handle, C.byref(st)))
     return st.as_dict()
+
+
+RESULT_FIELDS = ("count", "s0", "s1", "mix", "tc", "sum")
+
+
+def smap_result_reduce(plan: Plan, dst, stream=None):
+    """Asynchronously reduce the last run's results into `dst`, a DEVICE tensor
+    of 6 int64 (count, s0, s1, mix, tc, bits of the fp64 sum) -- ready for an
+    all-reduce of dst[:5] (exact mod 2^64) and dst[5:].view(float64)."""
+    _check(_lib.smap_result_reduce(plan.handle, _ptr(dst), _stream(stream)))
+
+
+def result_dict(rec) -> dict:
+    """Host view of a 6 x int64 result record."""
+    import numpy as np
+    a = rec.cpu().numpy() if hasattr(rec, "cpu") else np.asarray(rec)
+    u = a.view(np.uint64)
+    d = dict(zip(RESULT_FIELDS[:5], (int(x) for x in u[:5])))
+    d["sum"] = float(a[5:6].view(np.float64)[0])
+    return d
 
 
 # ------------------------------------------------------------------ torch conveniences

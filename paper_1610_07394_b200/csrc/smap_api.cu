@@ -28,6 +28,8 @@ struct smap_plan_s {
     uint64_t npartials = 0;
     double *d_scratch = nullptr;
     float *d_stage = nullptr;
+    smap_result *d_rec = nullptr;   // smap_run_host: device record
+    smap_result *h_rec = nullptr;   // smap_run_host: pinned host record
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t last_stream = nullptr;
     uint32_t last_launches = 0;
@@ -102,8 +104,8 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
             return fail(SMAP_E_INVALID, "THREAD granularity needs rho^m <= 1024 (rho=%d, m=%d)", rho, m);
         if (d->persistent) return fail(SMAP_E_INVALID, "persistent CTAs need TILE granularity");
     } else {
-        const bool ok = m == 2 ? (rho == 32 || rho == 64 || rho == 128) : (rho == 8 || rho == 16 || rho == 32);
-        if (!ok) return fail(SMAP_E_INVALID, "TILE rho must be in %s (got %d)", m == 2 ? "{32,64,128}" : "{8,16,32}", rho);
+        const bool ok = m == 2 ? (rho == 32 || rho == 64 || rho == 128 || rho == 256) : (rho == 8 || rho == 16 || rho == 32);
+        if (!ok) return fail(SMAP_E_INVALID, "TILE rho must be in %s (got %d)", m == 2 ? "{32,64,128,256}" : "{8,16,32}", rho);
         if (d->persistent < 0) return fail(SMAP_E_INVALID, "persistent must be >= 0");
     }
     const int64_t N = n / rho;
@@ -113,6 +115,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (!lam && G != 1) return fail(SMAP_E_INVALID, "BB plans are unsharded");
     if (lam && (N / 2) % G != 0) return fail(SMAP_E_INVALID, "shard_count %d does not divide N/2 = %lld", G, (long long)(N / 2));
     if (d->shard_rank < 0 || d->shard_rank >= G) return fail(SMAP_E_INVALID, "shard_rank out of range");
+    if (d->order != SMAP_ORDER_ROWS && d->order != SMAP_ORDER_SQUARES) return fail(SMAP_E_INVALID, "bad order %d", d->order);
 
     smap_plan_s *p = new (std::nothrow) smap_plan_s();
     if (!p) return fail(SMAP_E_NOMEM, "host allocation failed");
@@ -122,6 +125,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     P.n = (int)n; P.N = (int)N; P.log2N = ilog2(N); P.rho = rho; P.log2rho = ilog2(rho);
     if (lam) {
         P.W = (int)(N / 2 / G); P.log2W = ilog2(P.W); P.wx0 = d->shard_rank * P.W;
+        P.order = m == 2 ? d->order : 0;
         P.nblocks = m == 2 ? (uint64_t)P.W * (uint64_t)(incl ? N + 1 : N)
                            : (uint64_t)P.W * (uint64_t)(N / 2) * (uint64_t)(3 * N / 4);
     } else {
@@ -301,6 +305,16 @@ smap_status smap_stats_fetch(smap_plan_t p, smap_stats *st)
     return SMAP_OK;
 }
 
+smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream)
+{
+    if (!p || !dst) return fail(SMAP_E_INVALID, "smap_result_reduce: NULL argument");
+    if ((reinterpret_cast<uintptr_t>(dst) & 7) != 0) return fail(SMAP_E_INVALID, "smap_result_reduce: dst not 8-byte aligned");
+    if (!p->ran) return fail(SMAP_E_INVALID, "smap_result_reduce before smap_run");
+    cudaError_t e = launch_result_reduce(p->d_res, reinterpret_cast<smap_result *>(dst), (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "result reduce launch");
+    return SMAP_OK;
+}
+
 smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, float param, void *out,
                           size_t out_bytes, uint32_t flags, void *stream, smap_stats *stats)
 {
@@ -315,9 +329,18 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
     }
     smap_status st = smap_run(p, pl, dev_pts, param, out, out_bytes, flags, stream);
     if (st != SMAP_OK) return st;
-    CK(cudaMemcpyAsync(p->h_res, p->d_res, sizeof(Result), cudaMemcpyDeviceToHost, s));
+    if (!p->d_rec) CK(cudaMalloc(&p->d_rec, sizeof(smap_result)));
+    if (!p->h_rec) CK(cudaMallocHost(&p->h_rec, sizeof(smap_result)));
+    cudaError_t e = launch_result_reduce(p->d_res, p->d_rec, s);
+    if (e != cudaSuccess) return cuda_fail(e, "result reduce launch");
+    CK(cudaMemcpyAsync(p->h_rec, p->d_rec, sizeof(smap_result), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    fill_stats(p, p->h_res, stats);
+    smap_plan_query(p, stats);
+    stats->count = p->h_rec->count; stats->s0 = p->h_rec->s0; stats->s1 = p->h_rec->s1;
+    stats->mix = p->h_rec->mix; stats->tc = p->h_rec->tc; stats->sum = p->h_rec->sum;
+    stats->launches = p->last_launches + 1;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p->ev0, p->ev1) == cudaSuccess) stats->kernel_ms = ms;
     return SMAP_OK;
 }
 
@@ -329,6 +352,8 @@ void smap_destroy(smap_plan_t p)
     if (p->d_partials) cudaFree(p->d_partials);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_stage) cudaFree(p->d_stage);
+    if (p->d_rec) cudaFree(p->d_rec);
+    if (p->h_rec) cudaFreeHost(p->h_rec);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     delete p;
@@ -362,6 +387,30 @@ __global__ void __launch_bounds__(1024) k_fin2(const double *in, uint64_t n, Res
 }
 
 uint64_t finalize_scratch_elems(uint64_t np) { return (np + kFin1Per - 1) / kFin1Per; }
+
+// Sum the kSlots integer slots (exact mod 2^64) and copy the fp64 sum into
+// one 48-byte smap_result record.
+__global__ void __launch_bounds__(32) k_result_reduce(const Result *res, smap_result *dst)
+{
+    const int lane = threadIdx.x;
+    uint64_t v[5];
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+        uint64_t s = 0;
+        for (int i = lane; i < kSlots; i += 32) s += res->slot[i][k];
+        v[k] = warp_sum_u64(s);
+    }
+    if (lane == 0) {
+        dst->count = v[0]; dst->s0 = v[1]; dst->s1 = v[2]; dst->mix = v[3]; dst->tc = v[4];
+        dst->sum = res->sum;
+    }
+}
+
+cudaError_t launch_result_reduce(const Result *res, smap_result *dst, cudaStream_t s)
+{
+    k_result_reduce<<<1, 32, 0, s>>>(res, dst);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res, cudaStream_t s,
                             uint32_t *launches)

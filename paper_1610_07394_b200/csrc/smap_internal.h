@@ -28,7 +28,8 @@ struct Params {
     int W;          // grid columns of this shard = N / (2G)   (BB: N)
     int log2W;
     int wx0;        // first column of this shard = rank * W
-    uint64_t nblocks;              // blocks / tiles in this shard's grid
+    int order;      // lambda2 launch order: 0 rows, 1 level squares
+    uint64_t nblocks;             // blocks / tiles in this shard's grid
     const float *pts;              // n x 3 fp32 AoS (EDM / ATM / TC)
     float param;                   // ATM eps^2, TC R
     void *out;
@@ -47,5 +48,11 @@ cudaError_t launch_tile3(const Params &P, int T, bool lam, int pl, int cs, unsig
 cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res,
                             cudaStream_t s, uint32_t *launches);
 uint64_t finalize_scratch_elems(uint64_t np);
+}  // namespace smap
+
+#include "smap.h"
+
+namespace smap {
+cudaError_t launch_result_reduce(const Result *res, smap_result *dst, cudaStream_t s);
 
 } // namespace smap

@@ -46,11 +46,12 @@ def u32(t):
 @pytest.mark.parametrize("gran,rho,ns", [("thread", 4, [8, 16, 64, 512, 4096]), ("tile", 32, [64, 256, 2048])])
 @pytest.mark.parametrize("map_", ["lambda", "bb"])
 @pytest.mark.parametrize("diag", ["strict", "inclusive"])
-def test_map_dump_m2(sm, orc, gran, rho, ns, map_, diag):
+@pytest.mark.parametrize("order", ["rows", "squares"])
+def test_map_dump_m2(sm, orc, gran, rho, ns, map_, diag, order):
     for n in ns:
-        plan = sm.smap_plan(2, n, rho, map=map_, diag=diag, granularity=gran)
+        plan = sm.smap_plan(2, n, rho, map=map_, diag=diag, granularity=gran, order=order)
         out, _ = run(sm, plan, "map_dump")
-        exp = orc.map_dump(2, diag == "inclusive", map_ == "bb", n // rho)
+        exp = orc.map_dump(2, diag == "inclusive", map_ == "bb", n // rho, order=order)
         np.testing.assert_array_equal(out.cpu().numpy().reshape(-1, 4), exp)
 
 
@@ -68,11 +69,11 @@ def test_map_dump_m3(sm, orc, gran, rho, ns, map_):
 
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_map_dump_sharded(sm, orc, G):
-    for m, n, rho in [(2, 256, 4), (3, 128, 2)]:
+    for m, n, rho, order in [(2, 256, 4, "rows"), (2, 256, 4, "squares"), (2, 64, 1, "squares"), (3, 128, 2, "rows")]:
         for r in range(G):
-            plan = sm.smap_plan(m, n, rho, shard_rank=r, shard_count=G)
+            plan = sm.smap_plan(m, n, rho, shard_rank=r, shard_count=G, order=order)
             out, _ = run(sm, plan, "map_dump")
-            exp = orc.map_dump(m, False, False, n // rho, rank=r, G=G)
+            exp = orc.map_dump(m, False, False, n // rho, rank=r, G=G, order=order)
             np.testing.assert_array_equal(out.cpu().numpy().reshape(-1, 4), exp)
 
 
@@ -84,10 +85,12 @@ CASES3 = [(16, 2), (64, 4), (64, 8), (128, 8), (256, 8)]
 @pytest.mark.parametrize("n,rho", CASES2)
 @pytest.mark.parametrize("map_", ["lambda", "bb"])
 @pytest.mark.parametrize("diag", ["strict", "inclusive"])
-def test_thread_dump_m2(sm, orc, n, rho, map_, diag):
-    plan = sm.smap_plan(2, n, rho, map=map_, diag=diag)
+@pytest.mark.parametrize("order", ["rows", "squares"])
+def test_thread_dump_m2(sm, orc, n, rho, map_, diag, order):
+    plan = sm.smap_plan(2, n, rho, map=map_, diag=diag, order=order)
     out, _ = run(sm, plan, "thread_dump")
-    np.testing.assert_array_equal(u64(out), orc.thread_dump(2, diag == "inclusive", map_ == "bb", n, rho))
+    np.testing.assert_array_equal(u64(out), orc.thread_dump(2, diag == "inclusive", map_ == "bb", n, rho,
+                                                              order=order))
 
 
 @pytest.mark.parametrize("n,rho", CASES3)
@@ -144,20 +147,37 @@ def test_index_write_m3(sm, orc, gran, rho, map_):
         assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
 
 
-@pytest.mark.parametrize("gran,rho", [("thread", 16), ("thread", 32), ("tile", 32), ("tile", 64), ("tile", 128)])
+@pytest.mark.parametrize("gran,rho", [("thread", 16), ("thread", 32), ("tile", 32), ("tile", 64), ("tile", 128),
+                                      ("tile", 256)])
 @pytest.mark.parametrize("map_", ["lambda", "bb"])
-@pytest.mark.parametrize("pts", ["uniform", "duplicates"])
+@pytest.mark.parametrize("pts", ["uniform", "duplicates", "tiny", "huge"])
 def test_edm_bit_exact(sm, orc, gran, rho, map_, pts):
+    """Bit-exact fp32 EDM, with and without the fused checksum (different kernel
+    paths).  Edge inputs: exact duplicates (r^2 = 0), tiny coordinates (r^2
+    below the fast-sqrt range, denormal squares) and huge coordinates (r^2
+    overflow to inf) exercise the exact-path fallbacks."""
     n = 2048
-    p = workloads.points(n, workloads.SEED_C2) if pts == "uniform" else workloads.clustered_points(n, 5)
+    if pts == "uniform":
+        p = workloads.points(n, workloads.SEED_C2)
+    elif pts == "duplicates":
+        p = workloads.clustered_points(n, 5)
+    elif pts == "tiny":
+        p = (workloads.points(n, 6) * np.float32(1e-30)).astype(np.float32)
+    else:
+        p = workloads.points(n, 8)
+        p[::97] *= np.float32(3e19)
     plan = sm.smap_plan(2, n, rho, map=map_, granularity=gran)
-    out, st = run(sm, plan, "edm", points=dev_points(p), flags=sm.RUN_CHECKSUM_MIX)
     exp = orc.edm(p)
-    got = out.cpu().numpy()
-    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), \
-        f"{(got.view(np.uint32) != exp.view(np.uint32)).sum()} mismatching elements"
     cs = orc.cs_array(exp)
-    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+    for flags in (0, sm.RUN_CHECKSUM, sm.RUN_CHECKSUM_MIX):
+        out, st = run(sm, plan, "edm", points=dev_points(p), flags=flags)
+        got = out.cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), \
+            f"flags={flags}: {(got.view(np.uint32) != exp.view(np.uint32)).sum()} mismatching elements"
+        if flags:
+            assert (st["count"], st["s0"], st["s1"]) == (cs["count"], cs["s0"], cs["s1"]), flags
+        if flags & sm.RUN_CHECKSUM_MIX:
+            assert st["mix"] == cs["mix"]
 
 
 @pytest.mark.parametrize("gran,rho", [("thread", 8), ("tile", 8), ("tile", 16), ("tile", 32)])
@@ -217,6 +237,31 @@ def test_shards_partition_exactly(sm, G, gran, m, n, rho):
     plan = sm.smap_plan(m, n, rho, granularity=gran)
     _, st = run(sm, plan, "index_write", flags=sm.RUN_CHECKSUM_MIX)
     assert all(st[k] == tot[k] for k in tot)
+
+
+# ---------------------------------------------------------------- device result record + host-buffer API
+def test_result_reduce_and_run_host(sm, orc):
+    n = 1024
+    p = workloads.points(n, 4)
+    exp = orc.cs_array(orc.edm(p))
+    plan = sm.smap_plan(2, n, 128, granularity="tile")
+    out = sm.alloc_out(plan, "edm")
+    sm.smap_run(plan, "edm", points=dev_points(p), out=out, flags=sm.RUN_CHECKSUM_MIX)
+    rec = torch.zeros(6, dtype=torch.int64, device="cuda")
+    sm.smap_result_reduce(plan, rec)
+    r = sm.result_dict(rec)
+    assert (r["count"], r["s0"], r["s1"], r["mix"]) == (exp["count"], exp["s0"], exp["s1"], exp["mix"])
+    pinned = torch.from_numpy(p).pin_memory()
+    out.zero_()
+    st = sm.smap_run_host(plan, "edm", host_points=pinned, out=out, flags=sm.RUN_CHECKSUM)
+    assert (st["count"], st["s0"], st["s1"]) == (exp["count"], exp["s0"], exp["s1"])
+    assert st["launches"] == 2
+    # ATM through the record: fp64 field
+    p3 = workloads.points(128, 5)
+    plan3 = sm.smap_plan(3, 128, 16, granularity="tile")
+    st3 = sm.smap_run_host(plan3, "atm", host_points=p3, param=1e-2)
+    ref = orc.atm_sum(p3, np.float32(1e-2))
+    assert abs(st3["sum"] - ref) <= 1e-5 * abs(ref)
 
 
 # ---------------------------------------------------------------- closed forms vs launch
