@@ -66,7 +66,7 @@ typedef enum {
     /* one rho^m TILE of elements per 256-thread CTA step: lambda is applied to
      * tiles (the same map, coarser blocks); threads loop over the tile rows
      * with lanes on the contiguous axis; diagonal tiles are clipped per row
-     * instead of folded.  m=2: rho in {32,64,128,256}; m=3: rho in {8,16,32}. */
+     * instead of folded.  m=2: rho in {32,64,128,256,512}; m=3: rho in {8,16,32}. */
     SMAP_GRAN_TILE = 1
 } smap_granularity;
 
@@ -80,6 +80,8 @@ typedef enum {
     SMAP_PAYLOAD_THREAD_DUMP = 6, /* THREAD gran. only: uint64 per launched thread, p or UINT64_MAX */
     SMAP_PAYLOAD_EMPTY = 7        /* decode only, no element work (block-scheduling microbenchmark) */
 } smap_payload;
+
+#define SMAP_DEVICE_NONE (-2)      /* smap_plan_desc.device: host-only plan */
 
 /* smap_run flags */
 #define SMAP_RUN_CHECKSUM     0x1u /* INDEX_WRITE/EDM: accumulate s0, s1 (E21) */
@@ -97,7 +99,8 @@ typedef struct {
     int     persistent;   /* TILE only: 0 = one CTA per tile; k > 0 = k CTAs per SM looping over tiles */
     int     shard_rank;   /* 0 .. shard_count-1 */
     int     shard_count;  /* G: power of two dividing N/2 (lambda only); 1 = unsharded */
-    int     device;       /* CUDA device ordinal; -1 = the calling thread's current device */
+    int     device;       /* CUDA device ordinal; -1 = the calling thread's current device;
+                             SMAP_DEVICE_NONE = host-only plan (validation + closed forms; cannot run) */
     int     order;        /* lambda2 launch order (smap_order); ignored otherwise */
 } smap_plan_desc;
 

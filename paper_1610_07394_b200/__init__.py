@@ -29,6 +29,7 @@ GRAN = {"thread": 0, "tile": 1}
 ORDER = {"rows": 0, "squares": 1}
 PAYLOAD = {"index_write": 0, "edm": 1, "atm": 2, "tc": 3, "map_dump": 4, "hitcount": 5,
            "thread_dump": 6, "empty": 7}
+DEVICE_NONE = -2          # smap_plan(device=DEVICE_NONE): host-only plan (validation + closed forms)
 RUN_CHECKSUM = 0x1
 RUN_CHECKSUM_MIX = 0x2
 

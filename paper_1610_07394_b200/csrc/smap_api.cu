@@ -104,8 +104,8 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
             return fail(SMAP_E_INVALID, "THREAD granularity needs rho^m <= 1024 (rho=%d, m=%d)", rho, m);
         if (d->persistent) return fail(SMAP_E_INVALID, "persistent CTAs need TILE granularity");
     } else {
-        const bool ok = m == 2 ? (rho == 32 || rho == 64 || rho == 128 || rho == 256) : (rho == 8 || rho == 16 || rho == 32);
-        if (!ok) return fail(SMAP_E_INVALID, "TILE rho must be in %s (got %d)", m == 2 ? "{32,64,128,256}" : "{8,16,32}", rho);
+        const bool ok = m == 2 ? (rho >= 32 && rho <= 512) : (rho == 8 || rho == 16 || rho == 32);
+        if (!ok) return fail(SMAP_E_INVALID, "TILE rho must be in %s (got %d)", m == 2 ? "{32,...,512}" : "{8,16,32}", rho);
         if (d->persistent < 0) return fail(SMAP_E_INVALID, "persistent must be >= 0");
     }
     const int64_t N = n / rho;
@@ -140,6 +140,12 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     p->elem64 = p->V > ((uint64_t)1 << 32);
 
     int dev = d->device;
+    if (dev == SMAP_DEVICE_NONE) {            // host-only plan: validation + closed forms, no device work
+        p->device = dev;
+        p->ctas = 0;
+        *out = p;
+        return SMAP_OK;
+    }
     if (dev < 0) {
         cudaError_t e = cudaGetDevice(&dev);
         if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaGetDevice"); }
@@ -217,6 +223,7 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
 {
     g_err.clear();
     if (!p) return fail(SMAP_E_INVALID, "smap_run: NULL plan");
+    if (p->device == SMAP_DEVICE_NONE) return fail(SMAP_E_INVALID, "smap_run on a host-only plan");
     const int ipl = internal_pl(p, pl);
     if (ipl < 0) return fail(SMAP_E_INVALID, "unknown payload %d", (int)pl);
     const smap_plan_desc &d = p->d;
@@ -298,7 +305,7 @@ static void fill_stats(smap_plan_t p, const Result *r, smap_stats *st)
 smap_status smap_stats_fetch(smap_plan_t p, smap_stats *st)
 {
     if (!p || !st) return fail(SMAP_E_INVALID, "smap_stats_fetch: NULL argument");
-    if (!p->ran) return fail(SMAP_E_INVALID, "smap_stats_fetch before smap_run");
+    if (!p->ran) return fail(SMAP_E_INVALID, "smap_stats_fetch before smap_run (or on a host-only plan)");
     CK(cudaEventSynchronize(p->ev1));
     CK(cudaMemcpy(p->h_res, p->d_res, sizeof(Result), cudaMemcpyDeviceToHost));
     fill_stats(p, p->h_res, st);
@@ -308,6 +315,7 @@ smap_status smap_stats_fetch(smap_plan_t p, smap_stats *st)
 smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream)
 {
     if (!p || !dst) return fail(SMAP_E_INVALID, "smap_result_reduce: NULL argument");
+    if (p->device == SMAP_DEVICE_NONE) return fail(SMAP_E_INVALID, "smap_result_reduce on a host-only plan");
     if ((reinterpret_cast<uintptr_t>(dst) & 7) != 0) return fail(SMAP_E_INVALID, "smap_result_reduce: dst not 8-byte aligned");
     if (!p->ran) return fail(SMAP_E_INVALID, "smap_result_reduce before smap_run");
     cudaError_t e = launch_result_reduce(p->d_res, reinterpret_cast<smap_result *>(dst), (cudaStream_t)stream);
@@ -319,6 +327,7 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
                           size_t out_bytes, uint32_t flags, void *stream, smap_stats *stats)
 {
     if (!p || !stats) return fail(SMAP_E_INVALID, "smap_run_host: NULL argument");
+    if (p->device == SMAP_DEVICE_NONE) return fail(SMAP_E_INVALID, "smap_run_host on a host-only plan");
     cudaStream_t s = (cudaStream_t)stream;
     const float *dev_pts = nullptr;
     if (host_points) {

@@ -49,16 +49,16 @@ def main():
         p = torch.from_numpy(workloads.points(n, workloads.SEED_C2)).cuda()
         V = n * (n - 1) // 2
         out = torch.empty(V, dtype=torch.float32, device="cuda")
-        for cfg in [dict(rho=16, granularity="thread"), dict(rho=16, granularity="thread", order="squares"),
-                    dict(rho=128, granularity="tile"), dict(rho=128, granularity="tile", order="squares"),
+        for cfg in [dict(rho=128, granularity="tile"), dict(rho=128, granularity="tile", order="squares"),
                     dict(rho=256, granularity="tile"), dict(rho=256, granularity="tile", order="squares"),
-                    dict(rho=64, granularity="tile", order="squares"),
-                    dict(rho=128, granularity="tile", persistent=8, order="squares")]:
+                    dict(rho=512, granularity="tile"), dict(rho=512, granularity="tile", order="squares"),
+                    dict(rho=256, granularity="tile", persistent=4),
+                    dict(rho=512, granularity="tile", persistent=4)]:
             for mp in ("lambda", "bb"):
                 if mp == "bb" and cfg.get("order") == "squares":
                     continue
                 plan = sm.smap_plan(2, n, map=mp, **cfg)
-                for flags in (0,):
+                for flags in (0, 1):
                     ms = time_run(plan, "edm", pts=p, out=out, flags=flags)
                     rec(f"edm-{mp}-cs{flags}", 2, n, cfg, "edm", ms, V, 4)
         del out
