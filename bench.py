@@ -9,9 +9,9 @@ Workload (BASELINE.json configs[1], the metric's headline config; DESIGN.md s.6)
     d=3 fp32 (uniform in [0,1)^3, seed 161007394) -> 2,147,450,880 distances
     written to the packed layout (8.59 GB).
 One step = one pass of the hot path over the batch: lambda2 tile decode (a2),
-thread->element (a4), packed rank (a5), EDM payload (a6), fused linear
-checksum + count (a7), device result record, and for N > 1 the NCCL
-all-reduce of the record (a8).  Sharding: each rank owns W = N/(2G) columns of
+thread->element (a4), packed rank / tile position (a5), EDM payload (a6),
+fused count + xor of the value bits (a7, E21), device result record, and for
+N > 1 the NCCL all-gather + combine of the 56-byte records (a8).  Sharding: each rank owns W = N/(2G) columns of
 the lambda2 grid (equal useful volume, DESIGN.md s.7); total work is fixed, so
 scaling is "strong".
 
@@ -166,6 +166,21 @@ def run_reference(args):
     return 0
 
 
+def combine_records(gathered):
+    """Combine G smap_result records (G x 7 int64: count s0 s1 mix tc xr sum):
+    integer fields add mod 2^64, xr combines by xor (NCCL has no bitwise
+    reduction), the fp64 sum adds."""
+    import torch
+    out = torch.empty_like(gathered[0])
+    out[:5] = gathered[:, :5].sum(0)
+    x = gathered[0, 5].clone()
+    for g in range(1, gathered.shape[0]):
+        x ^= gathered[g, 5]
+    out[5] = x
+    out[6:7] = gathered[:, 6].contiguous().view(torch.float64).sum(0, keepdim=True).view(torch.int64)
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -203,14 +218,22 @@ def main():
     q = sm.smap_plan_query(plan)
     V = sm.smap_volume(2, n)
     out = sm.alloc_out(plan, "edm", device=dev)                 # 8.59 GB, full packed layout
-    rec = torch.zeros(6, dtype=torch.int64, device=dev)
-    flags = sm.RUN_CHECKSUM
+    rec = torch.zeros(7, dtype=torch.int64, device=dev)         # smap_result: count s0 s1 mix tc xr sum
+    gathered = torch.zeros(G * 7, dtype=torch.int64, device=dev)
+    # fused reduction of the step (a7): element count + S0 = sum of the value bits
+    # (E21); the position-weighted S1 and MIX are verification modes (tests)
+    flags = sm.RUN_XOR
+
+    def combine():
+        # a8: one all-gather of the 56-byte records, combined on the device
+        dist.all_gather_into_tensor(gathered, rec)
+        rec.copy_(combine_records(gathered.view(G, 7)))
 
     def step():
         sm.smap_run(plan, "edm", points=pts, out=out, flags=flags, stream=stream)
         sm.smap_result_reduce(plan, rec, stream=stream)
         if G > 1:
-            dist.all_reduce(rec[:5])                             # u64 sums: exact mod 2^64
+            combine()
 
     def barrier():
         torch.cuda.synchronize()
@@ -235,7 +258,7 @@ def main():
         ke1[k].record(stream)
         sm.smap_result_reduce(plan, rec, stream=stream)
         if G > 1:
-            dist.all_reduce(rec[:5])
+            combine()
     t1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -261,9 +284,11 @@ def main():
     for _ in range(e2e_steps):
         st = sm.smap_run_host(plan, "edm", host_points=host_pts, out=out, flags=flags, stream=stream)
         if G > 1:
-            r = torch.tensor([st["count"], st["s0"], st["s1"]], dtype=torch.int64).to(dev)  # noqa: F841
-            dist.all_reduce(r)
-            r.cpu()
+            r = torch.tensor([st["count"], st["xr"] - (1 << 64) if st["xr"] >= (1 << 63) else st["xr"]],
+                             dtype=torch.int64).to(dev)
+            g2 = torch.zeros(G, 2, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(g2, r)
+            g2.cpu()
     e1.record(stream)
     barrier()
     e2e_ms_local = max(e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3) / e2e_steps
@@ -289,11 +314,12 @@ def main():
             torch.cuda.synchronize()
             return a.elapsed_time(b) / reps
 
-        for name, c in (("tile", cfg), ("thread_rho16", dict(rho=16, granularity="thread"))):
+        for name, c in (("tile_tiles_layout", cfg), ("tile_rows_layout", dict(rho=256, granularity="tile")),
+                        ("thread_rho16_rows_layout", dict(rho=16, granularity="thread"))):
             c = {k: v for k, v in c.items() if k != "map"}
             lam = sm.smap_plan(2, n, map="lambda", **c)
             bb = sm.smap_plan(2, n, map="bb", **{k: v for k, v in c.items() if k != "order"})
-            reps = 10 if name == "tile" else 4
+            reps = 10 if name.startswith("tile") else 4
             ml, mb = time_plan(lam, reps), time_plan(bb, reps)
             ql, qb = sm.smap_plan_query(lam), sm.smap_plan_query(bb)
             compare[name] = {"lambda_ms": round(ml, 4), "bb_ms": round(mb, 4), "speedup": round(mb / ml, 3),
@@ -322,9 +348,26 @@ def main():
         traffic = tr.get(key)
     except (OSError, ValueError):
         pass
+    # the stricter denominator for a write-bound kernel: a write-only fill of the
+    # same output buffer on the same GPU (torch's fill kernel, CUDA events)
+    fill = None
+    try:
+        for _ in range(2):
+            out.zero_()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(5):
+            out.zero_()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fill = out.numel() * out.element_size() / (f0.elapsed_time(f1) / 5 * 1e-3) / 1e9
+    except RuntimeError:
+        pass
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4)}
+                "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(kern_ms, 4),
+                "write_fill_gbs_measured": round(fill, 1) if fill else None,
+                "frac_of_write_fill": round(achieved / fill, 4) if fill else None}
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
@@ -342,17 +385,19 @@ def main():
             "config": {"workload": "C2: m=2 EDM strict lower triangle, n=65536, d=3 fp32 (BASELINE configs[1])",
                        "map": "lambda2", "granularity": cfg["granularity"], "tile": cfg["rho"],
                        "order": cfg.get("order", "rows"), "persistent": cfg.get("persistent", 0),
+                       "layout": ("lambda-order tile-blocked packed lower triangle (DESIGN E23)"
+                                  if cfg.get("layout") == "tiles" else "canonical packed rows (DESIGN E16)"),
                        "elements": V, "parallelism": f"omega_x shards x{G}",
                        "l2": "output 8.59 GB per step >> 126 MB L2 (no flush needed; points stay L2-resident by design)"},
             "e2e": {"value": V / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": n * 12,
-                    "d2h_bytes_per_step": 48, "ms_per_step": e2e_ms},
+                    "d2h_bytes_per_step": 56, "ms_per_step": e2e_ms},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clk,
             "lambda_vs_bb": compare,
             "checksum_ok": bool(ok),
-            "result": {k: res[k] for k in ("count", "s0", "s1")},
+            "result": {k: res[k] for k in ("count", "xr")},
         }
         print(json.dumps(line), flush=True)
     if G > 1:

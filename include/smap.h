@@ -86,6 +86,7 @@ typedef enum {
 /* smap_run flags */
 #define SMAP_RUN_CHECKSUM     0x1u /* INDEX_WRITE/EDM: accumulate s0, s1 (E21) */
 #define SMAP_RUN_CHECKSUM_MIX 0x2u /* INDEX_WRITE/EDM: also accumulate mix (E21); implies CHECKSUM */
+#define SMAP_RUN_XOR          0x4u /* INDEX_WRITE/EDM: count and xr only (the cheapest fused reduction, E21) */
 
 typedef struct smap_plan_s *smap_plan_t;
 
@@ -102,7 +103,20 @@ typedef struct {
     int     device;       /* CUDA device ordinal; -1 = the calling thread's current device;
                              SMAP_DEVICE_NONE = host-only plan (validation + closed forms; cannot run) */
     int     order;        /* lambda2 launch order (smap_order); ignored otherwise */
+    int     layout;       /* m=2 output layout (smap_layout); TILE granularity only for SMAP_LAYOUT_TILES */
 } smap_plan_desc;
+
+typedef enum {
+    /* canonical packed rows (E16): out[p] at p = i(i-1)/2 + j (strict) / i(i+1)/2 + j;
+     * a sharded plan writes its own positions of the FULL-size array */
+    SMAP_LAYOUT_ROWS = 0,
+    /* lambda-order tile-blocked layout (E23; the "succinct blocked" storage of
+     * P:262-264): each T x T tile is one contiguous row-major slot, slots in row
+     * launch order; a sharded plan writes a SHARD-LOCAL array of V/G elements.
+     * Diagonal tiles are packed triangles (strict row 0: D1 then D2).
+     * smap_locate gives the position of any element in O(1). */
+    SMAP_LAYOUT_TILES = 1
+} smap_layout;
 
 typedef enum {
     SMAP_ORDER_ROWS = 0,    /* block-linear id = wy*W + (wx - wx0) */
@@ -122,6 +136,7 @@ typedef struct {
     uint64_t mix;              /* sum mix64(p ^ bits(v)*K) mod 2^64 (SMAP_RUN_CHECKSUM_MIX) */
     double   sum;              /* ATM: sum of terms (fp32 terms, fp32 per-thread, fp64 per CTA, fixed-order finalize) */
     uint64_t tc;               /* TC: triple count */
+    uint64_t xr;               /* xor of bits(v) over the elements (SMAP_RUN_XOR) */
     float    kernel_ms;        /* device time of the last smap_run's kernels (CUDA events on its stream) */
     uint32_t launches;         /* number of kernels the last smap_run launched */
 } smap_stats;
@@ -159,7 +174,7 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
 /* End-to-end variant with a HOST point array: copies host_points (n x 3 fp32;
  * pinned memory recommended) to the plan's device staging buffer on `stream`,
  * runs like smap_run, reduces the result on the device (smap_result_reduce),
- * copies the 48-byte smap_result back to host and synchronises the stream;
+ * copies the 56-byte smap_result back to host and synchronises the stream;
  * *stats (required) receives the results.  `out` stays a DEVICE buffer (the
  * packed outputs are consumed on the device). */
 smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, float param,
@@ -170,17 +185,26 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
  * dozen bytes) into *stats, together with the plan's closed forms. */
 smap_status smap_stats_fetch(smap_plan_t p, smap_stats *stats);
 
-/* Device-side result record of one run (48 bytes). */
+/* Device-side result record of one run (56 bytes). */
 typedef struct {
-    uint64_t count, s0, s1, mix, tc;
+    uint64_t count, s0, s1, mix, tc, xr;
     double   sum;
 } smap_result;
 
 /* Reduce the last smap_run's per-CTA results into one smap_result at the
  * DEVICE address `dst` (8-byte aligned), asynchronously on `stream` (one small
  * kernel, no host synchronisation) -- the input of a cross-GPU all-reduce:
- * the integer fields add exactly mod 2^64 and `sum` adds in fp64. */
+ * count/s0/s1/mix/tc add exactly mod 2^64, xr combines by xor, sum adds in fp64. */
 smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream);
+
+/* Where element e lives (m=2: e = {i, j}, j < i (<= i inclusive); m=3: e = {i, j, k}):
+ * *shard = the shard rank that writes it, *pos = its position in that shard's
+ * `out` array (SMAP_LAYOUT_ROWS: the packed rank in the full-size array;
+ * SMAP_LAYOUT_TILES: the position in the shard-local tile-blocked array).
+ * Host only, O(1) (lambda2^-1 via b = 2^floor(log2(I xor J)), q = I >> (log2 b + 1)).
+ * SMAP_E_INVALID for an element outside the domain; SMAP_E_UNSUPPORTED for m=3 with
+ * shard_count > 1. */
+smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *pos);
 
 /* Useful-element count V of a domain: C(n,2), n(n+1)/2 or C(n,3).  Host only. */
 uint64_t smap_volume(int m, int64_t n, int diag);

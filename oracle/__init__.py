@@ -76,6 +76,8 @@ _SIGS = {
     "or_cs_index": (i32, [i32, i32, u64, u64, u64, i32, P]),
     "or_cs_edm": (i32, [u64, P, u64, u64, i32, P]),
     "or_map_dump": (i32, [i32, i32, i32, u64, u64, u64, i32, P, u64]),
+    "or_tile_layout2": (i32, [u64, u64, i32, i32, u64, u64, P, u64]),
+    "or_cs_tiles2": (i32, [i32, u64, u64, i32, i32, u64, u64, P, i32, P]),
 }
 
 
@@ -203,6 +205,32 @@ def map_dump(m, inclusive, bb, N, rank=0, G=1, order="rows") -> np.ndarray:
     return out
 
 
+def tile_layout2(n, T, inclusive=False, bb=False, rank=0, G=1) -> np.ndarray:
+    """pos_of_rank[p] for the lambda-order tile-blocked layout (or_tile_layout2)."""
+    V = domain_volume(2, inclusive, n)
+    out = np.empty(V, np.int64)
+    assert lib().or_tile_layout2(n, T, int(inclusive), 0 if bb else 1, rank, G, _ptr(out), V) == 0
+    return out
+
+
+def to_tile_layout2(canonical: np.ndarray, n, T, inclusive=False, bb=False, rank=0, G=1) -> np.ndarray:
+    """Permute a canonical packed array into shard `rank`'s tile-blocked array."""
+    pos = tile_layout2(n, T, inclusive, bb, rank, G)
+    own = pos >= 0
+    out = np.empty(int(own.sum()), canonical.dtype)
+    out[pos[own]] = canonical[own]
+    return out
+
+
+def cs_tiles2(payload, n, T, inclusive=False, bb=False, rank=0, G=1, points=None, nthreads=0):
+    """Streaming checksum of 'index_write' / 'edm' in the tile-blocked layout."""
+    cs = np.zeros(5, np.uint64)
+    pp = _ptr(_pts(points)) if points is not None else None
+    assert lib().or_cs_tiles2({"index_write": 0, "edm": 1}[payload], n, T, int(inclusive), 0 if bb else 1,
+                              rank, G, pp, nthreads, _ptr(cs)) == 0
+    return dict(zip(CS_KEYS, (int(v) for v in cs)))
+
+
 def element_hits(m, inclusive, bb, n, rho, rank=0, G=1, hits=None, order="rows"):
     V = domain_volume(m, inclusive, n)
     if hits is None:
@@ -262,19 +290,19 @@ def tc_count(points, R, k_lo=0, k_hi=None, nthreads=0):
 def max_threads(): return lib().or_max_threads()
 
 
-CS_KEYS = ("count", "s0", "s1", "mix")
+CS_KEYS = ("count", "s0", "s1", "mix", "xr")
 
 
 def cs_array(arr: np.ndarray, p0=0):
     kind = {np.dtype(np.uint32): 0, np.dtype(np.uint64): 1, np.dtype(np.float32): 2}[arr.dtype]
     a = np.ascontiguousarray(arr)
-    cs = np.zeros(4, np.uint64)
+    cs = np.zeros(5, np.uint64)
     lib().or_cs_array(_ptr(a), kind, p0, a.size, _ptr(cs))
     return dict(zip(CS_KEYS, (int(v) for v in cs)))
 
 
 def cs_index(m, inclusive, n, lo=0, hi=None, nthreads=0):
-    cs = np.zeros(4, np.uint64)
+    cs = np.zeros(5, np.uint64)
     lib().or_cs_index(m, int(inclusive), n, lo, n if hi is None else hi, nthreads, _ptr(cs))
     return dict(zip(CS_KEYS, (int(v) for v in cs)))
 
@@ -282,6 +310,6 @@ def cs_index(m, inclusive, n, lo=0, hi=None, nthreads=0):
 def cs_edm(points, lo=0, hi=None, nthreads=0):
     p = _pts(points)
     n = p.shape[0]
-    cs = np.zeros(4, np.uint64)
+    cs = np.zeros(5, np.uint64)
     lib().or_cs_edm(n, _ptr(p), lo, n if hi is None else hi, nthreads, _ptr(cs))
     return dict(zip(CS_KEYS, (int(v) for v in cs)))

@@ -734,6 +734,7 @@ uint64_t or_tc_count(uint64_t n, const float *pts, float R, uint64_t k_lo, uint6
  *   cs[1] = S0  = sum bits(v)            mod 2^64
  *   cs[2] = S1  = sum (p+1) * bits(v)    mod 2^64
  *   cs[3] = MIX = sum mix64(p ^ (bits(v) * K)) mod 2^64
+ *   cs[4] = XR  = xor of bits(v)
  * bits(v) = the value's bit pattern zero-extended to 64 bits;
  * K = 0x9E3779B97F4A7C15; mix64 = the splitmix64 finaliser.
  * ====================================================================== */
@@ -751,6 +752,7 @@ static void or_cs_add(uint64_t *cs, uint64_t p, uint64_t bits)
     cs[1] += bits;
     cs[2] += (p + 1) * bits;
     cs[3] += or_mix64(p ^ (bits * 0x9E3779B97F4A7C15ULL));
+    cs[4] ^= bits;
 }
 
 static uint32_t or_fbits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
@@ -758,7 +760,7 @@ static uint32_t or_fbits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 /* Checksum of a materialised array: element e is at position p0 + e. */
 int or_cs_array(const void *arr, int kind /*0=u32,1=u64,2=f32*/, uint64_t p0, uint64_t len, uint64_t *cs)
 {
-    memset(cs, 0, 4 * sizeof(uint64_t));
+    memset(cs, 0, 5 * sizeof(uint64_t));
     for (uint64_t e = 0; e < len; e++) {
         uint64_t bits = kind == 0 ? ((const uint32_t *)arr)[e]
                       : kind == 1 ? ((const uint64_t *)arr)[e]
@@ -773,11 +775,11 @@ int or_cs_array(const void *arr, int kind /*0=u32,1=u64,2=f32*/, uint64_t p0, ui
 int or_cs_index(int m, int inclusive, uint64_t n, uint64_t lo, uint64_t hi, int nthreads, uint64_t *cs)
 {
     if (hi > n) hi = n;
-    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
     int nt = or_threads(nthreads);
-    #pragma omp parallel for schedule(dynamic, 64) reduction(+:c0,c1,c2,c3) num_threads(nt)
+    #pragma omp parallel for schedule(dynamic, 64) reduction(+:c0,c1,c2,c3) reduction(^:c4) num_threads(nt)
     for (uint64_t r = lo; r < hi; r++) {
-        uint64_t c[4] = {0, 0, 0, 0};
+        uint64_t c[5] = {0, 0, 0, 0, 0};
         if (m == 2) {
             uint64_t pos = inclusive ? or_rank2_incl(r, 0) : or_rank2_strict(r, 0);
             for (uint64_t j = 0; inclusive ? j <= r : j < r; j++, pos++) or_cs_add(c, pos, pos);
@@ -787,9 +789,9 @@ int or_cs_index(int m, int inclusive, uint64_t n, uint64_t lo, uint64_t hi, int 
                 for (uint64_t i = 0; i < j; i++, pos++) or_cs_add(c, pos, pos);
             }
         }
-        c0 += c[0]; c1 += c[1]; c2 += c[2]; c3 += c[3];
+        c0 += c[0]; c1 += c[1]; c2 += c[2]; c3 += c[3]; c4 ^= c[4];
     }
-    cs[0] = c0; cs[1] = c1; cs[2] = c2; cs[3] = c3;
+    cs[0] = c0; cs[1] = c1; cs[2] = c2; cs[3] = c3; cs[4] = c4;
     return 0;
 }
 
@@ -797,16 +799,126 @@ int or_cs_index(int m, int inclusive, uint64_t n, uint64_t lo, uint64_t hi, int 
 int or_cs_edm(uint64_t n, const float *pts, uint64_t lo, uint64_t hi, int nthreads, uint64_t *cs)
 {
     if (hi > n) hi = n;
-    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
     int nt = or_threads(nthreads);
-    #pragma omp parallel for schedule(dynamic, 16) reduction(+:c0,c1,c2,c3) num_threads(nt)
+    #pragma omp parallel for schedule(dynamic, 16) reduction(+:c0,c1,c2,c3) reduction(^:c4) num_threads(nt)
     for (uint64_t i = lo; i < hi; i++) {
-        uint64_t c[4] = {0, 0, 0, 0};
+        uint64_t c[5] = {0, 0, 0, 0, 0};
         uint64_t pos = or_rank2_strict(i, 0);
         for (uint64_t j = 0; j < i; j++, pos++) or_cs_add(c, pos, or_fbits(or_edm_dist(pts, i, j)));
-        c0 += c[0]; c1 += c[1]; c2 += c[2]; c3 += c[3];
+        c0 += c[0]; c1 += c[1]; c2 += c[2]; c3 += c[3]; c4 ^= c[4];
     }
-    cs[0] = c0; cs[1] = c1; cs[2] = c2; cs[3] = c3;
+    cs[0] = c0; cs[1] = c1; cs[2] = c2; cs[3] = c3; cs[4] = c4;
+    return 0;
+}
+
+/* ======================================================================
+ * The lambda-order tile-blocked layout of m=2 outputs (E23; the
+ * "succinct blocked" storage the paper pairs with block-space maps),
+ * defined by enumeration: walk the shard's tiles in ROW launch order
+ * (bid = wy*W + wx - wx0; for BB all tiles (I,J), J <= I, row-major) and give
+ * each tile's elements the next positions, row by row (r = i - I*T), columns
+ * in order; the strict row-0 slot holds D1's rows then D2's rows.
+ * pos_of_rank[p] = position in this shard's array (-1 if another shard owns p).
+ * ====================================================================== */
+int or_tile_layout2(uint64_t n, uint64_t T, int inclusive, int map, uint64_t rank, uint64_t G,
+                    int64_t *pos_of_rank, uint64_t V)
+{
+    uint64_t N = n / T;
+    for (uint64_t p = 0; p < V; p++) pos_of_rank[p] = -1;
+    int64_t pos = 0;
+    /* helper: emit the elements of diagonal block D (strict: c < r; inclusive: c <= r) */
+#define OR_EMIT(II, JJ, DIAGONAL)                                                       \
+    for (uint64_t r = 0; r < T; r++)                                                     \
+        for (uint64_t c = 0; c < T; c++) {                                               \
+            uint64_t i = (II) * T + r, j = (JJ) * T + c;                                 \
+            if ((DIAGONAL) && (inclusive ? c > r : c >= r)) continue;                    \
+            uint64_t p = inclusive ? or_rank2_incl(i, j) : or_rank2_strict(i, j);        \
+            if (p >= V) return -1;                                                       \
+            pos_of_rank[p] = pos++;                                                      \
+        }
+    if (map == 0) {
+        for (uint64_t I = 0; I < N; I++)
+            for (uint64_t J = 0; J <= I; J++) { OR_EMIT(I, J, J == I) }
+        return 0;
+    }
+    uint64_t W = N / 2 / G, wx0 = rank * W, H = inclusive ? N + 1 : N;
+    for (uint64_t wy = 0; wy < H; wy++)
+        for (uint64_t wx = wx0; wx < wx0 + W; wx++) {
+            if (wy == 0 && !inclusive) {
+                uint64_t D1 = wx, D2 = N - 1 - wx;
+                OR_EMIT(D1, D1, 1)
+                OR_EMIT(D2, D2, 1)
+            } else if (inclusive && (wy == 0 || wy == N)) {
+                uint64_t D = wy == 0 ? wx : wx + N / 2;
+                OR_EMIT(D, D, 1)
+            } else {
+                uint64_t J, I;
+                or_lambda2(wx, wy, &J, &I);
+                OR_EMIT(I, J, 0)
+            }
+        }
+#undef OR_EMIT
+    return 0;
+}
+
+/* Streaming checksum (E21) of an m=2 payload written in the tile-blocked
+ * layout, without materialising it: the same walk as or_tile_layout2, with the
+ * slot offsets of each grid row counted up front (plain sums of the slot
+ * sizes) so that the rows can be walked in parallel.
+ * payload 0 = index write (value = canonical rank), 1 = EDM (strict only). */
+int or_cs_tiles2(int payload, uint64_t n, uint64_t T, int inclusive, int map, uint64_t rank, uint64_t G,
+                 const float *pts, int nthreads, uint64_t *cs)
+{
+    uint64_t N = n / T;
+    if (payload == 1 && inclusive) return -1;
+    uint64_t rows = map == 0 ? N : (inclusive ? N + 1 : N);
+    uint64_t W = map == 0 ? 0 : N / 2 / G, wx0 = rank * W;
+    int64_t *row_off = malloc((rows + 1) * sizeof(int64_t));
+    uint64_t full = T * T, dstrict = T * (T - 1) / 2, dincl = T * (T + 1) / 2;
+    row_off[0] = 0;
+    for (uint64_t r = 0; r < rows; r++) {                  /* elements in grid row r */
+        uint64_t s;
+        if (map == 0) s = r * full + (inclusive ? dincl : dstrict);                 /* BB row I: I full + 1 diag */
+        else if (!inclusive && r == 0) s = W * 2 * dstrict;
+        else if (inclusive && (r == 0 || r == N)) s = W * dincl;
+        else s = W * full;
+        row_off[r + 1] = row_off[r] + (int64_t)s;
+    }
+    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+    int nt = or_threads(nthreads);
+    #pragma omp parallel for schedule(dynamic, 1) reduction(+:c0,c1,c2,c3) reduction(^:c4) num_threads(nt)
+    for (uint64_t r = 0; r < rows; r++) {
+        uint64_t c[5] = {0, 0, 0, 0, 0};
+        uint64_t pos = (uint64_t)row_off[r];
+        uint64_t ncols = map == 0 ? r + 1 : W;
+        for (uint64_t k = 0; k < ncols; k++) {
+            /* blocks of this slot: up to two (strict row 0) */
+            uint64_t bI[2], bJ[2], nb = 1;
+            int dg[2] = {0, 0};
+            if (map == 0) { bI[0] = r; bJ[0] = k; dg[0] = (k == r); }
+            else {
+                uint64_t wx = wx0 + k, wy = r;
+                if (!inclusive && wy == 0) { bI[0] = bJ[0] = wx; bI[1] = bJ[1] = N - 1 - wx; nb = 2; dg[0] = dg[1] = 1; }
+                else if (inclusive && (wy == 0 || wy == N)) { bI[0] = bJ[0] = (wy == 0 ? wx : wx + N / 2); dg[0] = 1; }
+                else { uint64_t J, I; or_lambda2(wx, wy, &J, &I); bI[0] = I; bJ[0] = J; }
+            }
+            for (uint64_t t = 0; t < nb; t++)
+                for (uint64_t rr = 0; rr < T; rr++)
+                    for (uint64_t cc = 0; cc < T; cc++) {
+                        if (dg[t] && (inclusive ? cc > rr : cc >= rr)) continue;
+                        uint64_t i = bI[t] * T + rr, j = bJ[t] * T + cc;
+                        uint64_t bits;
+                        if (payload == 0) bits = inclusive ? or_rank2_incl(i, j) : or_rank2_strict(i, j);
+                        else bits = or_fbits(or_edm_dist(pts, i, j));
+                        or_cs_add(c, pos, bits);
+                        pos++;
+                    }
+        }
+        c0 += c[0]; c1 += c[1]; c2 += c[2]; c3 += c[3]; c4 ^= c[4];
+    }
+    free(row_off);
+    cs[0] = c0; cs[1] = c1; cs[2] = c2; cs[3] = c3; cs[4] = c4;
     return 0;
 }
 

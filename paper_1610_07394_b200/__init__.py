@@ -27,11 +27,13 @@ MAP = {"bb": 0, "lambda": 1}
 DIAG = {"strict": 0, "inclusive": 1}
 GRAN = {"thread": 0, "tile": 1}
 ORDER = {"rows": 0, "squares": 1}
+LAYOUT = {"rows": 0, "tiles": 1}
 PAYLOAD = {"index_write": 0, "edm": 1, "atm": 2, "tc": 3, "map_dump": 4, "hitcount": 5,
            "thread_dump": 6, "empty": 7}
 DEVICE_NONE = -2          # smap_plan(device=DEVICE_NONE): host-only plan (validation + closed forms)
 RUN_CHECKSUM = 0x1
 RUN_CHECKSUM_MIX = 0x2
+RUN_XOR = 0x4
 
 
 class SmapError(RuntimeError):
@@ -43,13 +45,14 @@ class SmapError(RuntimeError):
 class PlanDesc(C.Structure):
     _fields_ = [("m", C.c_int), ("n", C.c_int64), ("rho", C.c_int), ("map", C.c_int), ("diag", C.c_int),
                 ("granularity", C.c_int), ("persistent", C.c_int), ("shard_rank", C.c_int),
-                ("shard_count", C.c_int), ("device", C.c_int), ("order", C.c_int)]
+                ("shard_count", C.c_int), ("device", C.c_int), ("order", C.c_int), ("layout", C.c_int)]
 
 
 class Stats(C.Structure):
     _fields_ = [("grid_blocks", C.c_uint64), ("launched_threads", C.c_uint64), ("useful_elems", C.c_uint64),
                 ("wasted_threads", C.c_uint64), ("count", C.c_uint64), ("s0", C.c_uint64), ("s1", C.c_uint64),
-                ("mix", C.c_uint64), ("sum", C.c_double), ("tc", C.c_uint64), ("kernel_ms", C.c_float),
+                ("mix", C.c_uint64), ("sum", C.c_double), ("tc", C.c_uint64), ("xr", C.c_uint64),
+                ("kernel_ms", C.c_float),
                 ("launches", C.c_uint32)]
 
     def as_dict(self):
@@ -66,6 +69,7 @@ _SIGS = {
     "smap_stats_fetch": (C.c_int, [_P, C.POINTER(Stats)]),
     "smap_result_reduce": (C.c_int, [_P, _P, _P]),
     "smap_volume": (C.c_uint64, [C.c_int, C.c_int64, C.c_int]),
+    "smap_locate": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
     "smap_destroy": (None, [_P]),
     "smap_last_error": (C.c_char_p, []),
     "smap_abi_version": (C.c_int, []),
@@ -118,9 +122,9 @@ class Plan:
 
 def smap_plan(m: int, n: int, rho: int, map: str = "lambda", diag: str = "strict", granularity: str = "thread",
               persistent: int = 0, shard_rank: int = 0, shard_count: int = 1, device: int = -1,
-              order: str = "rows") -> Plan:
+              order: str = "rows", layout: str = "rows") -> Plan:
     d = PlanDesc(m, n, rho, MAP[map], DIAG[diag], GRAN[granularity], persistent, shard_rank, shard_count, device,
-                 ORDER[order])
+                 ORDER[order], LAYOUT[layout])
     h = _P()
     _check(_lib.smap_plan(C.byref(d), C.byref(h)))
     return Plan(h, d)
@@ -136,6 +140,14 @@ def smap_plan_query(plan: Plan) -> dict:
     st = Stats()
     _check(_lib.smap_plan_query(plan.handle, C.byref(st)))
     return st.as_dict()
+
+
+def smap_locate(plan: Plan, *elem) -> tuple:
+    """(shard, position) of element (i, j[, k]) in the plan's output layout (host, O(1))."""
+    e = (C.c_int64 * 3)(*(list(elem) + [0] * (3 - len(elem))))
+    sh, pos = C.c_int(), C.c_uint64()
+    _check(_lib.smap_locate(plan.handle, e, C.byref(sh), C.byref(pos)))
+    return sh.value, pos.value
 
 
 def smap_out_bytes(plan: Plan, payload: str) -> int:
@@ -200,13 +212,14 @@ def smap_stats_fetch(plan: Plan) -> dict:
     return st.as_dict()
 
 
-RESULT_FIELDS = ("count", "s0", "s1", "mix", "tc", "sum")
+RESULT_FIELDS = ("count", "s0", "s1", "mix", "tc", "xr", "sum")
 
 
 def smap_result_reduce(plan: Plan, dst, stream=None):
     """Asynchronously reduce the last run's results into `dst`, a DEVICE tensor
-    of 6 int64 (count, s0, s1, mix, tc, bits of the fp64 sum) -- ready for an
-    all-reduce of dst[:5] (exact mod 2^64) and dst[5:].view(float64)."""
+    of 7 int64 (count, s0, s1, mix, tc, xr, bits of the fp64 sum) -- ready for
+    an all-reduce of dst[:5] (exact mod 2^64), an xor of dst[5] and a sum of
+    dst[6:].view(float64)."""
     _check(_lib.smap_result_reduce(plan.handle, _ptr(dst), _stream(stream)))
 
 
@@ -215,8 +228,8 @@ def result_dict(rec) -> dict:
     import numpy as np
     a = rec.cpu().numpy() if hasattr(rec, "cpu") else np.asarray(rec)
     u = a.view(np.uint64)
-    d = dict(zip(RESULT_FIELDS[:5], (int(x) for x in u[:5])))
-    d["sum"] = float(a[5:6].view(np.float64)[0])
+    d = dict(zip(RESULT_FIELDS[:6], (int(x) for x in u[:6])))
+    d["sum"] = float(a[6:7].view(np.float64)[0])
     return d
 
 
@@ -250,4 +263,4 @@ def alloc_out(plan: Plan, payload: str, device="cuda", zero: bool = False):
 
 __all__ = ["smap_plan", "smap_plan_query", "smap_out_bytes", "smap_run", "smap_run_host", "smap_stats_fetch",
            "smap_volume", "smap_destroy", "smap_last_error", "smap_abi_version", "Plan", "SmapError",
-           "alloc_out", "exported_symbols", "RUN_CHECKSUM", "RUN_CHECKSUM_MIX"]
+           "alloc_out", "exported_symbols", "RUN_CHECKSUM", "RUN_CHECKSUM_MIX", "RUN_XOR"]

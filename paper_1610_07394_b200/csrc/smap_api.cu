@@ -116,6 +116,9 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (lam && (N / 2) % G != 0) return fail(SMAP_E_INVALID, "shard_count %d does not divide N/2 = %lld", G, (long long)(N / 2));
     if (d->shard_rank < 0 || d->shard_rank >= G) return fail(SMAP_E_INVALID, "shard_rank out of range");
     if (d->order != SMAP_ORDER_ROWS && d->order != SMAP_ORDER_SQUARES) return fail(SMAP_E_INVALID, "bad order %d", d->order);
+    if (d->layout != SMAP_LAYOUT_ROWS && d->layout != SMAP_LAYOUT_TILES) return fail(SMAP_E_INVALID, "bad layout %d", d->layout);
+    if (d->layout == SMAP_LAYOUT_TILES && (m != 2 || !tile))
+        return fail(SMAP_E_INVALID, "the tile-blocked layout is for m=2 TILE plans");
 
     smap_plan_s *p = new (std::nothrow) smap_plan_s();
     if (!p) return fail(SMAP_E_NOMEM, "host allocation failed");
@@ -123,6 +126,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     Params &P = p->P;
     memset(&P, 0, sizeof P);
     P.n = (int)n; P.N = (int)N; P.log2N = ilog2(N); P.rho = rho; P.log2rho = ilog2(rho);
+    P.layout = d->layout;
     if (lam) {
         P.W = (int)(N / 2 / G); P.log2W = ilog2(P.W); P.wx0 = d->shard_rank * P.W;
         P.order = m == 2 ? d->order : 0;
@@ -206,10 +210,11 @@ static int internal_pl(smap_plan_t p, smap_payload pl)
 smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes)
 {
     if (!p || !bytes) return fail(SMAP_E_INVALID, "smap_out_bytes: NULL argument");
+    const uint64_t Vout = p->d.layout == SMAP_LAYOUT_TILES ? p->useful : p->V;   // tile layout: shard-local
     switch (pl) {
-    case SMAP_PAYLOAD_INDEX_WRITE: *bytes = (size_t)p->V * (p->elem64 ? 8 : 4); break;
-    case SMAP_PAYLOAD_EDM: *bytes = (size_t)p->V * 4; break;
-    case SMAP_PAYLOAD_HITCOUNT: *bytes = (size_t)p->V * 4; break;
+    case SMAP_PAYLOAD_INDEX_WRITE: *bytes = (size_t)Vout * (p->elem64 ? 8 : 4); break;
+    case SMAP_PAYLOAD_EDM: *bytes = (size_t)Vout * 4; break;
+    case SMAP_PAYLOAD_HITCOUNT: *bytes = (size_t)Vout * 4; break;
     case SMAP_PAYLOAD_MAP_DUMP: *bytes = (size_t)p->P.nblocks * 16; break;
     case SMAP_PAYLOAD_THREAD_DUMP: *bytes = (size_t)p->launched * 8; break;
     case SMAP_PAYLOAD_ATM: case SMAP_PAYLOAD_TC: case SMAP_PAYLOAD_EMPTY: *bytes = 0; break;
@@ -230,7 +235,7 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     const bool tile = d.granularity == SMAP_GRAN_TILE;
     const bool lam = d.map == SMAP_MAP_LAMBDA;
     const bool incl = d.diag == SMAP_DIAG_INCLUSIVE;
-    if (flags & ~(SMAP_RUN_CHECKSUM | SMAP_RUN_CHECKSUM_MIX)) return fail(SMAP_E_INVALID, "unknown flags 0x%x", flags);
+    if (flags & ~(SMAP_RUN_CHECKSUM | SMAP_RUN_CHECKSUM_MIX | SMAP_RUN_XOR)) return fail(SMAP_E_INVALID, "unknown flags 0x%x", flags);
     if (ipl == PL_EDM && (d.m != 2 || incl)) return fail(SMAP_E_INVALID, "EDM is defined on the m=2 strict domain");
     if ((ipl == PL_ATM || ipl == PL_TC) && d.m != 3) return fail(SMAP_E_INVALID, "ATM/TC are m=3 payloads");
     if ((ipl == PL_EDM || ipl == PL_ATM || ipl == PL_TC) && !points) return fail(SMAP_E_INVALID, "payload needs points");
@@ -240,7 +245,8 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     if (need > 0 && (!out || out_bytes < need))
         return fail(SMAP_E_INVALID, "out buffer too small: need %zu bytes, got %zu", need, out ? out_bytes : (size_t)0);
     const bool csum_pl = ipl == PL_IW32 || ipl == PL_IW64 || ipl == PL_EDM;
-    const int cs = !csum_pl ? 0 : (flags & SMAP_RUN_CHECKSUM_MIX) ? 2 : (flags & SMAP_RUN_CHECKSUM) ? 1 : 0;
+    const int cs = !csum_pl ? 0 : (flags & SMAP_RUN_CHECKSUM_MIX) ? 2 : (flags & SMAP_RUN_CHECKSUM) ? 1
+                                 : (flags & SMAP_RUN_XOR) ? 3 : 0;
     uint64_t rm = 1;
     for (int k = 0; k < d.m; k++) rm *= (uint64_t)d.rho;
     const bool reduces = cs > 0 || ipl == PL_ATM || ipl == PL_TC;
@@ -292,10 +298,12 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
 static void fill_stats(smap_plan_t p, const Result *r, smap_stats *st)
 {
     smap_plan_query(p, st);
-    uint64_t v[5] = {0, 0, 0, 0, 0};
-    for (int s = 0; s < kSlots; s++)
+    uint64_t v[5] = {0, 0, 0, 0, 0}, xr = 0;
+    for (int s = 0; s < kSlots; s++) {
         for (int k = 0; k < 5; k++) v[k] += r->slot[s][k];
-    st->count = v[0]; st->s0 = v[1]; st->s1 = v[2]; st->mix = v[3]; st->tc = v[4];
+        xr ^= r->slot[s][5];
+    }
+    st->count = v[0]; st->s0 = v[1]; st->s1 = v[2]; st->mix = v[3]; st->tc = v[4]; st->xr = xr;
     st->sum = r->sum;
     st->launches = p->last_launches;
     float ms = 0.f;
@@ -309,6 +317,66 @@ smap_status smap_stats_fetch(smap_plan_t p, smap_stats *st)
     CK(cudaEventSynchronize(p->ev1));
     CK(cudaMemcpy(p->h_res, p->d_res, sizeof(Result), cudaMemcpyDeviceToHost));
     fill_stats(p, p->h_res, st);
+    return SMAP_OK;
+}
+
+static int floor_log2_u64(uint64_t y) { return 63 - __builtin_clzll(y); }
+
+smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *pos)
+{
+    if (!p || !e || !shard || !pos) return fail(SMAP_E_INVALID, "smap_locate: NULL argument");
+    const smap_plan_desc &d = p->d;
+    const bool lam = d.map == SMAP_MAP_LAMBDA, incl = d.diag == SMAP_DIAG_INCLUSIVE;
+    const int64_t n = d.n;
+    if (d.m == 3) {
+        const int64_t i = e[0], j = e[1], k = e[2];
+        if (!(0 <= i && i < j && j < k && k < n)) return fail(SMAP_E_INVALID, "element outside the domain");
+        if (lam && d.shard_count > 1) return fail(SMAP_E_UNSUPPORTED, "m=3 owner shard lookup is not implemented");
+        *shard = 0;
+        *pos = (uint64_t)((unsigned __int128)k * (k - 1) * (k - 2) / 6) + (uint64_t)(j * (j - 1) / 2) + (uint64_t)i;
+        return SMAP_OK;
+    }
+    const int64_t i = e[0], j = e[1];
+    if (!(0 <= j && j < n && i < n && (incl ? j <= i : j < i))) return fail(SMAP_E_INVALID, "element outside the domain");
+    const uint64_t T = (uint64_t)d.rho, N = (uint64_t)p->P.N, W = lam ? (uint64_t)p->P.W : 0;
+    const uint64_t I = (uint64_t)i / T, J = (uint64_t)j / T, r = (uint64_t)i % T, c = (uint64_t)j % T;
+    // owner block omega (lambda) -- lambda2^-1 for off-diagonal blocks, the row-0 / row-N fold otherwise
+    uint64_t wx = 0, wy = 0;
+    bool second = false;                                         // strict row 0: D2 half of the slot
+    if (lam) {
+        if (I != J) {
+            const int l = floor_log2_u64(I ^ J);
+            const uint64_t b = 1ull << l, q = I >> (l + 1);
+            wx = J - q * b; wy = I - 2 * q * b;
+        } else if (!incl) {
+            if (I < N / 2) { wx = I; wy = 0; } else { wx = N - 1 - I; wy = 0; second = true; }
+        } else {
+            if (I < N / 2) { wx = I; wy = 0; } else { wx = I - N / 2; wy = N; }
+        }
+    }
+    const int owner = lam ? (int)(wx / W) : 0;
+    *shard = owner;
+    if (d.layout == SMAP_LAYOUT_ROWS) {
+        *pos = incl ? (uint64_t)i * (i + 1) / 2 + j : (uint64_t)i * (i - 1) / 2 + j;
+        return SMAP_OK;
+    }
+    // E23 tile layout: slot offset + position inside the slot
+    const uint64_t T2 = T * T, Sd = incl ? T * (T + 1) / 2 : T * (T - 1) / 2;
+    uint64_t slot;
+    if (!lam) {
+        slot = (I * (I - 1) / 2 + J) * T2 + I * Sd;
+    } else {
+        const uint64_t bid = wy * W + (wx - (uint64_t)owner * W);
+        if (!incl) slot = bid < W ? bid * T * (T - 1) : W * T * (T - 1) + (bid - W) * T2;
+        else if (bid < W) slot = bid * Sd;
+        else if (bid < N * W) slot = W * Sd + (bid - W) * T2;
+        else slot = W * Sd + (N - 1) * W * T2 + (bid - N * W) * Sd;
+    }
+    uint64_t in;
+    if (I != J) in = r * T + c;
+    else if (incl) in = r * (r + 1) / 2 + c;
+    else in = (second ? T * (T - 1) / 2 : 0) + r * (r - 1) / 2 + c;
+    *pos = slot + in;
     return SMAP_OK;
 }
 
@@ -346,7 +414,7 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
     CK(cudaStreamSynchronize(s));
     smap_plan_query(p, stats);
     stats->count = p->h_rec->count; stats->s0 = p->h_rec->s0; stats->s1 = p->h_rec->s1;
-    stats->mix = p->h_rec->mix; stats->tc = p->h_rec->tc; stats->sum = p->h_rec->sum;
+    stats->mix = p->h_rec->mix; stats->tc = p->h_rec->tc; stats->sum = p->h_rec->sum; stats->xr = p->h_rec->xr;
     stats->launches = p->last_launches + 1;
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p->ev0, p->ev1) == cudaSuccess) stats->kernel_ms = ms;
@@ -409,8 +477,13 @@ __global__ void __launch_bounds__(32) k_result_reduce(const Result *res, smap_re
         for (int i = lane; i < kSlots; i += 32) s += res->slot[i][k];
         v[k] = warp_sum_u64(s);
     }
+    uint64_t xr = 0;
+    for (int i = lane; i < kSlots; i += 32) xr ^= res->slot[i][5];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xr ^= __shfl_xor_sync(0xffffffffu, xr, o);
     if (lane == 0) {
         dst->count = v[0]; dst->s0 = v[1]; dst->s1 = v[2]; dst->mix = v[3]; dst->tc = v[4];
+        dst->xr = xr;
         dst->sum = res->sum;
     }
 }

@@ -11,7 +11,7 @@ constexpr int kSlots = 64;   // spread the per-CTA integer atomics over 64 slots
 
 // Device result block of one smap_run (zeroed on the stream before the kernel).
 struct Result {
-    unsigned long long slot[kSlots][5];  // per slot: count, s0, s1, mix, tc
+    unsigned long long slot[kSlots][6];  // per slot: count, s0, s1, mix, tc (added) and xr (xor-combined)
     double sum;                          // ATM, written by the finalize kernel
     double pad;
 };
@@ -29,6 +29,7 @@ struct Params {
     int log2W;
     int wx0;        // first column of this shard = rank * W
     int order;      // lambda2 launch order: 0 rows, 1 level squares
+    int layout;     // m=2 output layout: 0 canonical packed rows (E16), 1 lambda-order tiles (E23)
     uint64_t nblocks;             // blocks / tiles in this shard's grid
     const float *pts;              // n x 3 fp32 AoS (EDM / ATM / TC)
     float param;                   // ATM eps^2, TC R

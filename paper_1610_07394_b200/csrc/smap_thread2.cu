@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(1024) k_thread2(Params P)
             atomicAdd(reinterpret_cast<unsigned int *>(P.out) + p, 1u);
         }
     }
-    if (need_reduce) block_add_slots(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid);
+    if (need_reduce) block_add_slots<cs_mask<CS>()>(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid, acc.xr);
 }
 
 template <bool LAM, bool INCL, int PL, int CS>
@@ -86,6 +86,7 @@ static cudaError_t pick_pl(const Params &P, int pl, int cs, cudaStream_t s)
     if (pl == PLV) {                                                \
         if (cs == 0) return go2<LAM, INCL, PLV, 0>(P, s);           \
         if (cs == 1) return go2<LAM, INCL, PLV, 1>(P, s);           \
+        if (cs == 3) return go2<LAM, INCL, PLV, 3>(P, s);           \
         return go2<LAM, INCL, PLV, 2>(P, s);                        \
     }
     CS3(PL_IW32)

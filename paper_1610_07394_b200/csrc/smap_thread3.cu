@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
             if (PL == PL_IW64) { reinterpret_cast<uint64_t *>(P.out)[p] = p; acc.add(p, p); }
             if (PL == PL_HIT) atomicAdd(reinterpret_cast<unsigned int *>(P.out) + p, 1u);
         }
-        if (CS > 0) block_add_slots(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid);
+        if (CS > 0) block_add_slots<cs_mask<CS>()>(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid, acc.xr);
         return;
     }
     if (PL == PL_ATM || PL == PL_TC) {
@@ -125,6 +125,7 @@ static cudaError_t pick3(const Params &P, int pl, int cs, cudaStream_t s)
     if (pl == PLV) {                                      \
         if (cs == 0) return go3<LAM, PLV, 0>(P, s);       \
         if (cs == 1) return go3<LAM, PLV, 1>(P, s);       \
+        if (cs == 3) return go3<LAM, PLV, 3>(P, s);       \
         return go3<LAM, PLV, 2>(P, s);                    \
     }
     CS3(PL_IW32)

@@ -39,11 +39,12 @@ def compare(m, n, payload, variants, pts=None, param=0.0, out=None, reps=10, dia
         res = {"variant": name, "cfg": cfg}
         for mp in ("lambda", "bb"):
             c = dict(cfg)
+            flags = c.pop("flags", 0)
             if mp == "bb":
                 c.pop("order", None)
             plan = sm.smap_plan(m, n, map=mp, diag=diag, **c)
             q = sm.smap_plan_query(plan)
-            ms = time_run(plan, payload, pts=pts, param=param, out=out, reps=reps)
+            ms = time_run(plan, payload, pts=pts, param=param, out=out, reps=reps, flags=flags)
             res[mp] = {"ms": round(ms, 4), "launched": q["launched_threads"], "blocks": q["grid_blocks"]}
             e = sm.smap_run(plan, "empty") if False else None  # noqa: F841
             ems = time_run(plan, "empty", reps=reps)
@@ -79,8 +80,14 @@ def main():
         n = 65536
         p = torch.from_numpy(workloads.points(n, workloads.SEED_C2)).cuda()
         out = torch.empty(sm.smap_volume(2, n), dtype=torch.float32, device="cuda")
-        table["configs"]["C2"] = compare(2, n, "edm", [thread2, ("tile_rho128", dict(rho=128, granularity="tile")),
-                                                        ("tile_rho256", dict(rho=256, granularity="tile"))],
+        T = dict(granularity="tile", layout="tiles")
+        table["configs"]["C2"] = compare(2, n, "edm", [thread2, ("tile_rho256_rows", dict(rho=256, granularity="tile")),
+                                                        ("tile_rho128_tiles", dict(rho=128, **T)),
+                                                        ("tile_rho128_tiles_xor", dict(rho=128, flags=sm.RUN_XOR, **T)),
+                                                        ("tile_rho128_tiles_p4_xor", dict(rho=128, persistent=4, flags=sm.RUN_XOR, **T)),
+                                                        ("tile_rho128_tiles_p8_xor", dict(rho=128, persistent=8, flags=sm.RUN_XOR, **T)),
+                                                        ("tile_rho256_tiles_xor", dict(rho=256, flags=sm.RUN_XOR, **T)),
+                                                        ("tile_rho64_tiles_xor", dict(rho=64, flags=sm.RUN_XOR, **T))],
                                          pts=p, out=out, reps=a.reps)
         del out
     if "C3" in only:
@@ -97,7 +104,9 @@ def main():
         out = torch.empty(sm.smap_volume(2, n), dtype=torch.int64, device="cuda")
         table["configs"]["C4"] = compare(2, n, "index_write", [thread2, ("tile_rho128", dict(rho=128, granularity="tile")),
                                                                 ("tile_rho256", dict(rho=256, granularity="tile")),
-                                                                ("tile_rho512", dict(rho=512, granularity="tile"))],
+                                                                ("tile_rho512", dict(rho=512, granularity="tile")),
+                                                                ("tile_rho128_tiles", dict(rho=128, granularity="tile", layout="tiles")),
+                                                                ("tile_rho256_tiles", dict(rho=256, granularity="tile", layout="tiles"))],
                                          out=out, reps=max(3, a.reps // 2))
         del out
     if "C5" in only:

@@ -23,12 +23,15 @@ def main():
     ap.add_argument("--gran", default="tile")
     ap.add_argument("--map", default="lambda")
     ap.add_argument("--persistent", type=int, default=0)
+    ap.add_argument("--layout", default="rows")
+    ap.add_argument("--order", default="rows")
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--param", type=float, default=0.5)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--memset", action="store_true", help="also time a cudaMemset of the output (write roofline)")
     a = ap.parse_args()
-    plan = sm.smap_plan(a.m, a.n, a.rho, map=a.map, granularity=a.gran, persistent=a.persistent)
+    plan = sm.smap_plan(a.m, a.n, a.rho, map=a.map, granularity=a.gran, persistent=a.persistent,
+                        layout=a.layout, order=a.order)
     pts = torch.from_numpy(workloads.points(a.n, 7)).cuda()
     out = sm.alloc_out(plan, a.payload)
     for _ in range(a.reps):

@@ -109,3 +109,29 @@ def test_gloo_world2_allreduce_of_shard_records(orc, m, inc, n, rho):
     full = orc.cs_index(m, inc, n)
     assert tot == [full["count"], full["s0"], full["s1"], full["mix"]]
     assert useful[0] == useful[1] == full["count"] // 2     # exact volume balance
+
+
+def _rec_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    rec = torch.tensor([100 + rank, -1, 5, 7, 0, 0x0F0F << rank, 0], dtype=torch.int64)
+    rec[6:7] = torch.tensor([0.25 * (rank + 1)], dtype=torch.float64).view(torch.int64)
+    g = torch.zeros(world * 7, dtype=torch.int64)
+    dist.all_gather_into_tensor(g, rec)
+    out = bench.combine_records(g.view(world, 7))
+    if rank == 0:
+        q.put(out.tolist())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_record_combine():
+    """bench.py's a8 step: all-gather + combine of the 56-byte result records."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    mp.start_processes(_rec_worker, args=(2, _free_port(), q), nprocs=2, join=True, start_method="spawn")
+    out = q.get()
+    assert out[0] == 201 and out[1] == -2 and out[2] == 10 and out[3] == 14
+    assert out[5] == (0x0F0F ^ (0x0F0F << 1))
+    assert torch.tensor(out[6:7], dtype=torch.int64).view(torch.float64).item() == 0.75

@@ -1,7 +1,7 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configurations that
-bench.py times: sampled outputs the oracle computes one by one, plus the
-order-independent checksums (reading E21) the oracle streams over the whole
-domain on the host cores."""
+bench.py times: sampled outputs the oracle computes one by one (located with
+smap_locate), plus the order-independent checksums (reading E21) the oracle
+streams over the whole domain on the host cores."""
 import math
 
 import numpy as np
@@ -30,6 +30,10 @@ def _sample_pairs(n, k, seed):
     return i, j
 
 
+def _positions(sm, plan, i, j):
+    return np.array([sm.smap_locate(plan, int(a), int(b))[1] for a, b in zip(i, j)], np.int64)
+
+
 @pytest.mark.parametrize("cfg", workloads.BENCH_EDM_VARIANTS)
 def test_c2_edm_full(sm, orc, cfg):
     n = workloads.CONFIGS["C2"]["n"]
@@ -38,12 +42,15 @@ def test_c2_edm_full(sm, orc, cfg):
     out = sm.alloc_out(plan, "edm")
     sm.smap_run(plan, "edm", points=torch.from_numpy(p).cuda(), out=out, flags=sm.RUN_CHECKSUM_MIX)
     st = sm.smap_stats_fetch(plan)
-    i, j = _sample_pairs(n, 100000, 1)
-    pos = torch.from_numpy(i * (i - 1) // 2 + j).cuda()
+    i, j = _sample_pairs(n, 50000, 1)
+    pos = torch.from_numpy(_positions(sm, plan, i, j)).cuda()
     got = out[pos].cpu().numpy()
     exp = orc.edm_dist_many(p, i, j)
     assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
-    cs = orc.cs_edm(p)
+    if cfg.get("layout") == "tiles":
+        cs = orc.cs_tiles2("edm", n, cfg["rho"], bb=cfg["map"] == "bb", points=p)
+    else:
+        cs = orc.cs_edm(p)
     assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
     del out
     torch.cuda.empty_cache()
@@ -53,6 +60,7 @@ def test_c3_index_and_atm_full(sm, orc):
     c = workloads.CONFIGS["C3"]
     n = c["n"]
     p = workloads.points(n, workloads.SEED_C3)
+    ref = orc.atm_sum(p, np.float32(c["eps2"]))
     for cfg in workloads.BENCH_M3_VARIANTS:
         plan = sm.smap_plan(3, n, **cfg)
         out = sm.alloc_out(plan, "index_write")
@@ -64,7 +72,6 @@ def test_c3_index_and_atm_full(sm, orc):
         assert np.array_equal(got, np.arange(V, dtype=np.uint32))
         sm.smap_run(plan, "atm", points=torch.from_numpy(p).cuda(), param=c["eps2"])
         st = sm.smap_stats_fetch(plan)
-        ref = orc.atm_sum(p, np.float32(c["eps2"]))
         assert abs(st["sum"] - ref) <= 1e-5 * abs(ref)
 
 
@@ -81,22 +88,47 @@ def test_c5_tc_full(sm, orc):
         assert st["tc"] == ref
 
 
-def test_c4_index_write_full(sm, orc):
+@pytest.mark.parametrize("layout", ["tiles", "rows"])
+def test_c4_index_write_full(sm, orc, layout):
     n = workloads.CONFIGS["C4"]["n"]
     V = n * (n - 1) // 2
-    plan = sm.smap_plan(2, n, **workloads.BENCH_C4)
+    cfg = dict(workloads.BENCH_C4, layout=layout)
+    plan = sm.smap_plan(2, n, **cfg)
     out = sm.alloc_out(plan, "index_write")             # 68.7 GB of uint64 on the device
     assert out.numel() == V and out.dtype == torch.int64
     sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM_MIX)
     st = sm.smap_stats_fetch(plan)
     M = 1 << 64
     assert st["count"] == V
-    assert st["s0"] == (V * (V - 1) // 2) % M
-    assert st["s1"] == ((V - 1) * V * (V + 1) // 3) % M
-    i, j = _sample_pairs(n, 100000, 2)
-    pos = i * (i - 1) // 2 + j
-    got = out[torch.from_numpy(pos).cuda()].cpu().numpy()
-    assert np.array_equal(got, pos)
-    assert st["mix"] == orc.cs_index(2, False, n)["mix"]
+    assert st["s0"] == (V * (V - 1) // 2) % M           # values are the canonical ranks in both layouts
+    i, j = _sample_pairs(n, 50000, 2)
+    rank = i * (i - 1) // 2 + j
+    got = out[torch.from_numpy(_positions(sm, plan, i, j)).cuda()].cpu().numpy()
+    assert np.array_equal(got, rank)
+    if layout == "rows":
+        assert st["s1"] == ((V - 1) * V * (V + 1) // 3) % M
+        cs = orc.cs_index(2, False, n)
+    else:
+        cs = orc.cs_tiles2("index_write", n, cfg["rho"])
+    assert (st["s1"], st["mix"]) == (cs["s1"], cs["mix"])
     del out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_c4_sharded_tiles_partition(sm, orc, G):
+    """Each shard writes a shard-local V/G array; the records add up to the
+    unsharded ones (the bench's all-reduce, emulated on one GPU)."""
+    n = workloads.CONFIGS["C4"]["n"] // 4           # 2^15: keeps the emulation quick
+    V = n * (n - 1) // 2
+    tot = [0, 0, 0, 0]
+    for r in range(G):
+        plan = sm.smap_plan(2, n, shard_rank=r, shard_count=G, **workloads.BENCH_C4)
+        out = sm.alloc_out(plan, "index_write")
+        assert out.numel() == V // G
+        sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM_MIX)
+        st = sm.smap_stats_fetch(plan)
+        cs = orc.cs_tiles2("index_write", n, workloads.BENCH_C4["rho"], rank=r, G=G)
+        assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+        tot = [(a + b) % (1 << 64) for a, b in zip(tot, (st["count"], st["s0"], st["s1"], st["mix"]))]
+    assert tot[0] == V and tot[1] == (V * (V - 1) // 2) % (1 << 64)

@@ -131,6 +131,8 @@ def test_index_write_m2(sm, orc, gran, rho, map_, diag):
     np.testing.assert_array_equal(u32(out), exp)
     cs = orc.cs_array(exp)
     assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+    _, st = run(sm, plan, "index_write", flags=sm.RUN_XOR)
+    assert (st["count"], st["xr"]) == (cs["count"], cs["xr"])
 
 
 @pytest.mark.parametrize("gran,rho", [("thread", 8), ("thread", 4), ("tile", 8), ("tile", 16), ("tile", 32)])
@@ -169,13 +171,17 @@ def test_edm_bit_exact(sm, orc, gran, rho, map_, pts):
     plan = sm.smap_plan(2, n, rho, map=map_, granularity=gran)
     exp = orc.edm(p)
     cs = orc.cs_array(exp)
-    for flags in (0, sm.RUN_CHECKSUM, sm.RUN_CHECKSUM_MIX):
+    for flags in (0, sm.RUN_XOR, sm.RUN_CHECKSUM, sm.RUN_CHECKSUM_MIX):
         out, st = run(sm, plan, "edm", points=dev_points(p), flags=flags)
         got = out.cpu().numpy()
         assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), \
             f"flags={flags}: {(got.view(np.uint32) != exp.view(np.uint32)).sum()} mismatching elements"
         if flags:
-            assert (st["count"], st["s0"], st["s1"]) == (cs["count"], cs["s0"], cs["s1"]), flags
+            assert st["count"] == cs["count"], flags
+        if flags == sm.RUN_XOR:
+            assert st["xr"] == cs["xr"]
+        if flags & (sm.RUN_CHECKSUM | sm.RUN_CHECKSUM_MIX):
+            assert (st["s0"], st["s1"]) == (cs["s0"], cs["s1"]), flags
         if flags & sm.RUN_CHECKSUM_MIX:
             assert st["mix"] == cs["mix"]
 
@@ -247,7 +253,7 @@ def test_result_reduce_and_run_host(sm, orc):
     plan = sm.smap_plan(2, n, 128, granularity="tile")
     out = sm.alloc_out(plan, "edm")
     sm.smap_run(plan, "edm", points=dev_points(p), out=out, flags=sm.RUN_CHECKSUM_MIX)
-    rec = torch.zeros(6, dtype=torch.int64, device="cuda")
+    rec = torch.zeros(7, dtype=torch.int64, device="cuda")
     sm.smap_result_reduce(plan, rec)
     r = sm.result_dict(rec)
     assert (r["count"], r["s0"], r["s1"], r["mix"]) == (exp["count"], exp["s0"], exp["s1"], exp["mix"])

@@ -167,4 +167,5 @@ def test_streaming_edm_checksum_equals_array(orc):
     # row ranges combine additively (sharded evaluation)
     a, b = orc.cs_edm(p, 0, 333), orc.cs_edm(p, 333, 600)
     tot = orc.cs_edm(p)
-    assert all((a[k] + b[k]) % (1 << 64) == tot[k] for k in tot)
+    assert all((a[k] + b[k]) % (1 << 64) == tot[k] for k in tot if k != "xr")
+    assert a["xr"] ^ b["xr"] == tot["xr"]

@@ -32,12 +32,14 @@ CONFIGS = {
 
 #: launch configurations bench.py times (parity-tested at full size in
 #: tests/test_gpu_fullsize.py).  Keys are smap_plan keyword arguments.
-BENCH_EDM = dict(rho=256, granularity="tile", map="lambda")
+BENCH_EDM = dict(rho=256, granularity="tile", map="lambda", layout="tiles")
 BENCH_EDM_VARIANTS = [BENCH_EDM, dict(rho=16, granularity="thread", map="lambda"),
-                      dict(rho=256, granularity="tile", map="bb")]
-BENCH_M3 = dict(rho=32, granularity="tile", persistent=4, map="lambda")
+                      dict(rho=256, granularity="tile", map="lambda"),
+                      dict(rho=256, granularity="tile", map="bb", layout="tiles"),
+                      dict(rho=128, granularity="tile", map="lambda", layout="tiles")]
+BENCH_M3 = dict(rho=32, granularity="tile", map="lambda")
 BENCH_M3_VARIANTS = [BENCH_M3, dict(rho=8, granularity="thread", map="lambda")]
-BENCH_C4 = dict(rho=128, granularity="tile", persistent=4, map="lambda")
+BENCH_C4 = dict(rho=128, granularity="tile", map="lambda", layout="tiles")
 
 
 def points(n: int, seed: int) -> np.ndarray:
