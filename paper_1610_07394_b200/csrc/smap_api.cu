@@ -27,6 +27,7 @@ struct smap_plan_s {
     double *d_partials = nullptr;
     uint64_t npartials = 0;
     double *d_scratch = nullptr;
+    uint32_t *d_adj = nullptr;      // TC pair-predicate bitmap (TILE)
     float *d_stage = nullptr;
     smap_result *d_rec = nullptr;   // smap_run_host: device record
     smap_result *h_rec = nullptr;   // smap_run_host: pinned host record
@@ -257,6 +258,9 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     int cur = -1;
     CK(cudaGetDevice(&cur));
     if (cur != p->device) CK(cudaSetDevice(p->device));
+    const bool tc_bits = ipl == PL_TC && tile;
+    if (tc_bits && (d.n % 32) != 0) return fail(SMAP_E_UNSUPPORTED, "bit-sliced TC needs n to be a multiple of 32");
+    if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)d.n * (size_t)(d.n / 32) * sizeof(uint32_t)));
     if (ipl == PL_ATM) {
         const uint64_t np = tile ? p->ctas : p->P.nblocks;
         if (np > p->npartials) {
@@ -272,10 +276,16 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     P.param = param;
     P.out = out;
     P.partials = p->d_partials;
+    P.adj = p->d_adj;
     uint32_t launches = 0;
     CK(cudaMemsetAsync(p->d_res, 0, sizeof(Result), s));
     CK(cudaEventRecord(p->ev0, s));
     cudaError_t e;
+    if (tc_bits) {
+        cudaError_t ea = launch_tc_adjacency(points, (int)d.n, param, p->d_adj, s);
+        if (ea != cudaSuccess) return cuda_fail(ea, "TC adjacency launch");
+        launches++;
+    }
     if (!tile) e = d.m == 2 ? launch_thread2(P, lam, incl, ipl, cs, s) : launch_thread3(P, lam, ipl, cs, s);
     else e = d.m == 2 ? launch_tile2(P, d.rho, lam, incl, ipl, cs, p->ctas, s)
                       : launch_tile3(P, d.rho, lam, ipl, cs, p->ctas, s);
@@ -428,6 +438,7 @@ void smap_destroy(smap_plan_t p)
     if (p->h_res) cudaFreeHost(p->h_res);
     if (p->d_partials) cudaFree(p->d_partials);
     if (p->d_scratch) cudaFree(p->d_scratch);
+    if (p->d_adj) cudaFree(p->d_adj);
     if (p->d_stage) cudaFree(p->d_stage);
     if (p->d_rec) cudaFree(p->d_rec);
     if (p->h_rec) cudaFreeHost(p->h_rec);

@@ -36,6 +36,7 @@ struct Params {
     void *out;
     Result *res;
     double *partials;              // ATM: one fp64 per CTA
+    const uint32_t *adj;           // TC (TILE): pair-predicate bitmap, n rows of n/32 words
 };
 
 // Kernel launchers (one per translation unit).  Return cudaErrorInvalidValue
@@ -44,6 +45,9 @@ cudaError_t launch_thread2(const Params &P, bool lam, bool incl, int pl, int cs,
 cudaError_t launch_thread3(const Params &P, bool lam, int pl, int cs, cudaStream_t s);
 cudaError_t launch_tile2(const Params &P, int T, bool lam, bool incl, int pl, int cs, unsigned ctas, cudaStream_t s);
 cudaError_t launch_tile3(const Params &P, int T, bool lam, int pl, int cs, unsigned ctas, cudaStream_t s);
+// TC pre-pass: adj[j * (n/32) + w] bit b <=> r2(32w + b, j) < R*R (the same fp32
+// predicate as the per-triple compare); n a multiple of 32.
+cudaError_t launch_tc_adjacency(const float *pts, int n, float R, uint32_t *adj, cudaStream_t s);
 // Deterministic fixed-order fp64 reduction of partials[0..np) into res->sum.
 // Adds the number of kernels it launched to *launches.
 cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res,
