@@ -50,7 +50,13 @@ typedef enum {
 
 typedef enum {
     SMAP_MAP_BB = 0,         /* bounding box: identity + filter */
-    SMAP_MAP_LAMBDA = 1      /* lambda2 / lambda3 reading R3 */
+    SMAP_MAP_LAMBDA = 1,     /* lambda2 / lambda3 reading R3 */
+    SMAP_MAP_ENUM = 2        /* comparison baseline: the linear-enumeration map
+                                g: Z^1 -> Z^m of P:166-174, block-space as in P:252-262, inverted by
+                                the analytic root (fp32 sqrt for m=2, cbrt + sqrt for m=3, then an
+                                exact integer correction).  A 1-D grid of the N(N+1)/2 blocks J<=I
+                                (m=2) or the C(N+2,3) blocks I<=J<=K (m=3); diagonal blocks filter
+                                like BB.  THREAD granularity, unsharded. */
 } smap_map;
 
 typedef enum {
@@ -226,6 +232,7 @@ int smap_abi_version(void);
  * m=3 lambda: (x0,x1,x2) = (I,J,K) sorted block triple; cls 0 inside branch,
  *             1 reflected branch; cls 2 body-diagonal block x0 = d; cls 3 idle.
  * m=3 BB:     (I,J,K) = (wx,wy,wz); cls 0 I<J<K, 5 I=J<K, 6 I<J=K, 2 I=J=K, 4 outside.
+ * ENUM:       as BB (m=2 (J,I) cls 0/3; m=3 (I,J,K) cls 0/5/6/2), never outside.
  *
  * Launch order (block-linear id bid; W = N/(2G) columns per shard, wx0 = rank*W):
  *   lambda2, SMAP_ORDER_ROWS: bid = wy*W + (wx - wx0), wy in [0, N) strict / [0, N] inclusive
@@ -234,6 +241,7 @@ int smap_abi_version(void);
  *            wy = b + r / b, wx = wx0 + s*b + r mod b; else wy = b + t / W, wx = wx0 + t mod W
  *   lambda3: bid = (wz*(N/2) + wy)*W + (wx - wx0), wz in [0, 3N/4)
  *   BB2:     bid = I*N + J;   BB3: bid = (K*N + J)*N + I
+ *   ENUM2:   bid = I(I+1)/2 + J, J <= I;   ENUM3: bid = C(K+2,3) + C(J+1,2) + I, I <= J <= K
  * Threads (THREAD_DUMP order): t = ty*rho + tx (m=2); t = (c*rho + b)*rho + a (m=3). */
 
 #ifdef __cplusplus

@@ -169,20 +169,27 @@ def rank2_incl(i, j): return lib().or_rank2_incl(i, j)
 def rank3(i, j, k): return lib().or_rank3(i, j, k)
 
 
+def _mapc(bb) -> int:
+    """Map code: True/"bb" -> 0 (bounding box), False/"lambda" -> 1, "enum" -> 2."""
+    if isinstance(bb, str):
+        return {"bb": 0, "lambda": 1, "enum": 2}[bb]
+    return 0 if bb else 1
+
+
 def thread_elem2(inclusive, bb, N, rho, wx, wy, tx, ty):
     e = np.zeros(3, np.int64)
-    ok = lib().or_thread_elem2(int(inclusive), 0 if bb else 1, N, rho, wx, wy, tx, ty, _ptr(e))
+    ok = lib().or_thread_elem2(int(inclusive), _mapc(bb), N, rho, wx, wy, tx, ty, _ptr(e))
     return (int(e[0]), int(e[1])) if ok else None
 
 
 def thread_elem3(bb, N, rho, wx, wy, wz, a, b, c):
     e = np.zeros(3, np.int64)
-    ok = lib().or_thread_elem3(0 if bb else 1, N, rho, wx, wy, wz, a, b, c, _ptr(e))
+    ok = lib().or_thread_elem3(_mapc(bb), N, rho, wx, wy, wz, a, b, c, _ptr(e))
     return (int(e[0]), int(e[1]), int(e[2])) if ok else None
 
 
 def grid_blocks(m, inclusive, bb, N, G=1):
-    return lib().or_grid_blocks(m, int(inclusive), 0 if bb else 1, N, G)
+    return lib().or_grid_blocks(m, int(inclusive), _mapc(bb), N, G)
 
 
 ORDERS = {"rows": 0, "squares": 1}
@@ -192,7 +199,7 @@ def thread_dump(m, inclusive, bb, n, rho, rank=0, G=1, order="rows") -> np.ndarr
     N = n // rho
     length = grid_blocks(m, inclusive, bb, N, G) * rho ** m
     out = np.empty(length, np.uint64)
-    assert lib().or_thread_dump(m, int(inclusive), 0 if bb else 1, n, rho, rank, G, ORDERS[order],
+    assert lib().or_thread_dump(m, int(inclusive), _mapc(bb), n, rho, rank, G, ORDERS[order],
                                 _ptr(out), length) == 0
     return out
 
@@ -201,7 +208,7 @@ def map_dump(m, inclusive, bb, N, rank=0, G=1, order="rows") -> np.ndarray:
     """Expected MAP_DUMP records (int32 x 4 per grid block, launch order)."""
     nb = grid_blocks(m, inclusive, bb, N, G)
     out = np.empty((nb, 4), np.int32)
-    assert lib().or_map_dump(m, int(inclusive), 0 if bb else 1, N, rank, G, ORDERS[order], _ptr(out), nb) == 0
+    assert lib().or_map_dump(m, int(inclusive), _mapc(bb), N, rank, G, ORDERS[order], _ptr(out), nb) == 0
     return out
 
 
@@ -209,7 +216,7 @@ def tile_layout2(n, T, inclusive=False, bb=False, rank=0, G=1) -> np.ndarray:
     """pos_of_rank[p] for the lambda-order tile-blocked layout (or_tile_layout2)."""
     V = domain_volume(2, inclusive, n)
     out = np.empty(V, np.int64)
-    assert lib().or_tile_layout2(n, T, int(inclusive), 0 if bb else 1, rank, G, _ptr(out), V) == 0
+    assert lib().or_tile_layout2(n, T, int(inclusive), _mapc(bb), rank, G, _ptr(out), V) == 0
     return out
 
 
@@ -226,7 +233,7 @@ def cs_tiles2(payload, n, T, inclusive=False, bb=False, rank=0, G=1, points=None
     """Streaming checksum of 'index_write' / 'edm' in the tile-blocked layout."""
     cs = np.zeros(5, np.uint64)
     pp = _ptr(_pts(points)) if points is not None else None
-    assert lib().or_cs_tiles2({"index_write": 0, "edm": 1}[payload], n, T, int(inclusive), 0 if bb else 1,
+    assert lib().or_cs_tiles2({"index_write": 0, "edm": 1}[payload], n, T, int(inclusive), _mapc(bb),
                               rank, G, pp, nthreads, _ptr(cs)) == 0
     return dict(zip(CS_KEYS, (int(v) for v in cs)))
 
@@ -236,7 +243,7 @@ def element_hits(m, inclusive, bb, n, rho, rank=0, G=1, hits=None, order="rows")
     if hits is None:
         hits = np.zeros(V, np.uint32)
     r = np.zeros(3, np.int64)
-    assert lib().or_element_hits(m, int(inclusive), 0 if bb else 1, n, rho, rank, G, ORDERS[order],
+    assert lib().or_element_hits(m, int(inclusive), _mapc(bb), n, rho, rank, G, ORDERS[order],
                                  _ptr(hits), V, _ptr(r)) == 0
     return hits, dict(launched=int(r[0]), useful=int(r[1]), outside=int(r[2]))
 

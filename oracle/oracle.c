@@ -387,13 +387,16 @@ uint64_t or_domain_volume(int m, int inclusive, uint64_t n)
  * a4 -- thread -> element for the one-element-per-thread launch
  * (blocks of rho^m threads; readings E6, E14).
  * map: 0 = bounding box (identity + filter),
- *      1 = lambda.   Block coordinates (wx, wy, wz) are the paper's omega.
+ *      1 = lambda,
+ *      2 = enumeration baseline: the block coordinates come from
+ *          the linear block rank (or_block_coords), the threads filter like BB.
+ * Block coordinates (wx, wy, wz) are the paper's omega (BB / ENUM: the block).
  * Returns 1 and e[] = (i, j[, k]) for a useful thread, 0 for an idle one.
  * ====================================================================== */
 int or_thread_elem2(int inclusive, int map, uint64_t N, uint64_t rho,
                     uint64_t wx, uint64_t wy, uint64_t tx, uint64_t ty, int64_t *e)
 {
-    if (map == 0) {                               /* BB: block (J, I) = (wx, wy) */
+    if (map == 0 || map == 2) {                   /* BB / ENUM: block (J, I) = (wx, wy) */
         uint64_t i = wy * rho + ty, j = wx * rho + tx;
         if (inclusive ? (j <= i) : (j < i)) { e[0] = (int64_t)i; e[1] = (int64_t)j; return 1; }
         return 0;
@@ -423,7 +426,7 @@ int or_thread_elem2(int inclusive, int map, uint64_t N, uint64_t rho,
 int or_thread_elem3(int map, uint64_t N, uint64_t rho, uint64_t wx, uint64_t wy, uint64_t wz,
                     uint64_t a, uint64_t b, uint64_t c, int64_t *e)
 {
-    if (map == 0) {                               /* BB: block (I, J, K) = (wx, wy, wz) */
+    if (map == 0 || map == 2) {                   /* BB / ENUM: block (I, J, K) = (wx, wy, wz) */
         uint64_t i = wx * rho + a, j = wy * rho + b, k = wz * rho + c;
         if (i < j && j < k) { e[0] = (int64_t)i; e[1] = (int64_t)j; e[2] = (int64_t)k; return 1; }
         return 0;
@@ -454,6 +457,8 @@ int or_thread_elem3(int map, uint64_t N, uint64_t rho, uint64_t wx, uint64_t wy,
  *   lambda3:  bid = (wz*(N/2) + wy)*W + (wx - wx0), wz in [0, 3N/4)
  *   BB2:      bid = I*N + J      (wx = J, wy = I)
  *   BB3:      bid = (K*N + J)*N + I
+ *   ENUM2:    bid = row-major rank of the block (J, I) among J <= I
+ *   ENUM3:    bid = colex rank of the block (I, J, K) among I <= J <= K
  * with W = N/(2G) columns per shard and wx0 = rank*W; threads within a block
  * are t = ty*rho + tx (m=2) and t = (c*rho + b)*rho + a (m=3). */
 static uint64_t or_ipow(uint64_t b, int e) { uint64_t r = 1; while (e-- > 0) r *= b; return r; }
@@ -461,6 +466,7 @@ static uint64_t or_ipow(uint64_t b, int e) { uint64_t r = 1; while (e-- > 0) r *
 uint64_t or_grid_blocks(int m, int inclusive, int map, uint64_t N, uint64_t G)
 {
     if (map == 0) return or_ipow(N, m);
+    if (map == 2) return m == 2 ? N * (N + 1) / 2 : N * (N + 1) * (N + 2) / 6;
     if (m == 2) return (N / 2 / G) * (inclusive ? N + 1 : N);
     return (N / 2 / G) * (N / 2) * (3 * N / 4);
 }
@@ -474,6 +480,19 @@ static int or_block_coords(int m, int inclusive, int map, uint64_t N, uint64_t r
     (void)inclusive;
     if (map == 0) {
         for (int d = 0; d < m; d++) { w[d] = bid % N; bid /= N; }
+        return 0;
+    }
+    if (map == 2) {                  /* enumeration order, found by walking the rows (no roots) */
+        if (m == 2) {
+            uint64_t I = 0;
+            while (bid >= I + 1) { bid -= I + 1; I++; }           /* row I holds I + 1 blocks */
+            w[0] = bid; w[1] = I;
+            return 0;
+        }
+        uint64_t K = 0, J = 0;
+        while (bid >= (K + 1) * (K + 2) / 2) { bid -= (K + 1) * (K + 2) / 2; K++; }   /* layer K */
+        while (bid >= J + 1) { bid -= J + 1; J++; }
+        w[0] = bid; w[1] = J; w[2] = K;
         return 0;
     }
     uint64_t W = N / 2 / G, wx0 = rank * W;
@@ -936,7 +955,7 @@ int or_map_dump(int m, int inclusive, int map, uint64_t N, uint64_t rank, uint64
         or_block_coords(m, inclusive, map, N, rank, G, order, bid, w);
         int32_t *r = out + 4 * bid;
         r[0] = r[1] = r[2] = r[3] = 0;
-        if (m == 2 && map == 0) {
+        if (m == 2 && (map == 0 || map == 2)) {
             r[0] = (int32_t)w[0]; r[1] = (int32_t)w[1];
             r[3] = w[0] < w[1] ? 0 : (w[0] == w[1] ? 3 : 4);
         } else if (m == 2) {
@@ -944,7 +963,7 @@ int or_map_dump(int m, int inclusive, int map, uint64_t N, uint64_t rank, uint64
             else if (w[1] == 0) { r[0] = r[1] = (int32_t)w[0]; r[3] = 2; }
             else if (inclusive && w[1] == N) { r[0] = r[1] = (int32_t)(w[0] + N / 2); r[3] = 2; }
             else { uint64_t x, y; or_lambda2(w[0], w[1], &x, &y); r[0] = (int32_t)x; r[1] = (int32_t)y; r[3] = 0; }
-        } else if (map == 0) {
+        } else if (map == 0 || map == 2) {
             uint64_t I = w[0], J = w[1], K = w[2];
             r[0] = (int32_t)I; r[1] = (int32_t)J; r[2] = (int32_t)K;
             r[3] = (I < J && J < K) ? 0 : (I == J && J < K) ? 5 : (I < J && J == K) ? 6 : (I == J && J == K) ? 2 : 4;

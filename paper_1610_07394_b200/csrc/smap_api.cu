@@ -93,7 +93,10 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     const bool tile = d->granularity == SMAP_GRAN_TILE;
     const int G = d->shard_count;
     if (m != 2 && m != 3) return fail(SMAP_E_INVALID, "m must be 2 or 3 (got %d)", m);
-    if (d->map != SMAP_MAP_BB && d->map != SMAP_MAP_LAMBDA) return fail(SMAP_E_INVALID, "bad map %d", d->map);
+    if (d->map != SMAP_MAP_BB && d->map != SMAP_MAP_LAMBDA && d->map != SMAP_MAP_ENUM)
+        return fail(SMAP_E_INVALID, "bad map %d", d->map);
+    const bool enm = d->map == SMAP_MAP_ENUM;
+    if (enm && tile) return fail(SMAP_E_INVALID, "the enumeration baseline map is THREAD granularity only");
     if (d->diag != SMAP_DIAG_STRICT && d->diag != SMAP_DIAG_INCLUSIVE) return fail(SMAP_E_INVALID, "bad diag %d", d->diag);
     if (d->granularity != SMAP_GRAN_THREAD && d->granularity != SMAP_GRAN_TILE)
         return fail(SMAP_E_INVALID, "bad granularity %d", d->granularity);
@@ -113,7 +116,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (m == 2 && lam && N < 2) return fail(SMAP_E_INVALID, "lambda2 needs N = n/rho >= 2");
     if (m == 3 && lam && N < 8) return fail(SMAP_E_INVALID, "lambda3 needs N = n/rho >= 8 (body blocks, E14)");
     if (G < 1 || !is_pow2(G)) return fail(SMAP_E_INVALID, "shard_count must be a power of two >= 1");
-    if (!lam && G != 1) return fail(SMAP_E_INVALID, "BB plans are unsharded");
+    if (!lam && G != 1) return fail(SMAP_E_INVALID, "BB and ENUM plans are unsharded");
     if (lam && (N / 2) % G != 0) return fail(SMAP_E_INVALID, "shard_count %d does not divide N/2 = %lld", G, (long long)(N / 2));
     if (d->shard_rank < 0 || d->shard_rank >= G) return fail(SMAP_E_INVALID, "shard_rank out of range");
     if (d->order != SMAP_ORDER_ROWS && d->order != SMAP_ORDER_SQUARES) return fail(SMAP_E_INVALID, "bad order %d", d->order);
@@ -133,6 +136,9 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
         P.order = m == 2 ? d->order : 0;
         P.nblocks = m == 2 ? (uint64_t)P.W * (uint64_t)(incl ? N + 1 : N)
                            : (uint64_t)P.W * (uint64_t)(N / 2) * (uint64_t)(3 * N / 4);
+    } else if (enm) {                         // blocks J <= I (m=2) / I <= J <= K (m=3)
+        P.W = (int)N; P.log2W = P.log2N; P.wx0 = 0;
+        P.nblocks = m == 2 ? (uint64_t)N * (N + 1) / 2 : (uint64_t)N * (N + 1) * (N + 2) / 6;
     } else {
         P.W = (int)N; P.log2W = P.log2N; P.wx0 = 0;
         P.nblocks = m == 2 ? (uint64_t)N * N : (uint64_t)N * N * N;
@@ -286,7 +292,7 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
         if (ea != cudaSuccess) return cuda_fail(ea, "TC adjacency launch");
         launches++;
     }
-    if (!tile) e = d.m == 2 ? launch_thread2(P, lam, incl, ipl, cs, s) : launch_thread3(P, lam, ipl, cs, s);
+    if (!tile) e = d.m == 2 ? launch_thread2(P, d.map, incl, ipl, cs, s) : launch_thread3(P, d.map, ipl, cs, s);
     else e = d.m == 2 ? launch_tile2(P, d.rho, lam, incl, ipl, cs, p->ctas, s)
                       : launch_tile3(P, d.rho, lam, ipl, cs, p->ctas, s);
     if (e == cudaErrorInvalidValue) return fail(SMAP_E_UNSUPPORTED, "no kernel for this plan/payload combination");

@@ -41,8 +41,8 @@ struct Params {
 
 // Kernel launchers (one per translation unit).  Return cudaErrorInvalidValue
 // for a combination that has no instantiated kernel.
-cudaError_t launch_thread2(const Params &P, bool lam, bool incl, int pl, int cs, cudaStream_t s);
-cudaError_t launch_thread3(const Params &P, bool lam, int pl, int cs, cudaStream_t s);
+cudaError_t launch_thread2(const Params &P, int map, bool incl, int pl, int cs, cudaStream_t s);
+cudaError_t launch_thread3(const Params &P, int map, int pl, int cs, cudaStream_t s);
 cudaError_t launch_tile2(const Params &P, int T, bool lam, bool incl, int pl, int cs, unsigned ctas, cudaStream_t s);
 cudaError_t launch_tile3(const Params &P, int T, bool lam, int pl, int cs, unsigned ctas, cudaStream_t s);
 // TC pre-pass: adj[j * (n/32) + w] bit b <=> r2(32w + b, j) < R*R (the same fp32

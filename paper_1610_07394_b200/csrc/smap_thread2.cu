@@ -8,12 +8,13 @@
 
 namespace smap {
 
-template <bool LAM, bool INCL, int PL, int CS>
+template <int MAP, bool INCL, int PL, int CS>
 __global__ void __launch_bounds__(1024) k_thread2(Params P)
 {
+    constexpr bool LAM = MAP == SMAP_MAP_LAMBDA;
     const uint64_t bid = blockIdx.x;
     const uint32_t tx = threadIdx.x, ty = threadIdx.y, rho = (uint32_t)P.rho;
-    const Blk2 b = LAM ? decode_lambda2(bid, P, INCL) : decode_bb2(bid, P);
+    const Blk2 b = decode2<MAP>(bid, P, INCL);
 
     if (PL == PL_MAPD) {
         if (tx == 0 && ty == 0)
@@ -71,39 +72,40 @@ __global__ void __launch_bounds__(1024) k_thread2(Params P)
     if (need_reduce) block_add_slots<cs_mask<CS>()>(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid, acc.xr);
 }
 
-template <bool LAM, bool INCL, int PL, int CS>
+template <int MAP, bool INCL, int PL, int CS>
 static cudaError_t go2(const Params &P, cudaStream_t s)
 {
     dim3 block(P.rho, P.rho);
-    k_thread2<LAM, INCL, PL, CS><<<(unsigned)P.nblocks, block, 0, s>>>(P);
+    k_thread2<MAP, INCL, PL, CS><<<(unsigned)P.nblocks, block, 0, s>>>(P);
     return cudaGetLastError();
 }
 
-template <bool LAM, bool INCL>
+template <int MAP, bool INCL>
 static cudaError_t pick_pl(const Params &P, int pl, int cs, cudaStream_t s)
 {
 #define CS3(PLV)                                                    \
     if (pl == PLV) {                                                \
-        if (cs == 0) return go2<LAM, INCL, PLV, 0>(P, s);           \
-        if (cs == 1) return go2<LAM, INCL, PLV, 1>(P, s);           \
-        if (cs == 3) return go2<LAM, INCL, PLV, 3>(P, s);           \
-        return go2<LAM, INCL, PLV, 2>(P, s);                        \
+        if (cs == 0) return go2<MAP, INCL, PLV, 0>(P, s);           \
+        if (cs == 1) return go2<MAP, INCL, PLV, 1>(P, s);           \
+        if (cs == 3) return go2<MAP, INCL, PLV, 3>(P, s);           \
+        return go2<MAP, INCL, PLV, 2>(P, s);                        \
     }
     CS3(PL_IW32)
     CS3(PL_IW64)
     if (!INCL) { CS3(PL_EDM) }
 #undef CS3
-    if (pl == PL_MAPD) return go2<LAM, INCL, PL_MAPD, 0>(P, s);
-    if (pl == PL_HIT) return go2<LAM, INCL, PL_HIT, 0>(P, s);
-    if (pl == PL_TDUMP) return go2<LAM, INCL, PL_TDUMP, 0>(P, s);
-    if (pl == PL_EMPTY) return go2<LAM, INCL, PL_EMPTY, 0>(P, s);
+    if (pl == PL_MAPD) return go2<MAP, INCL, PL_MAPD, 0>(P, s);
+    if (pl == PL_HIT) return go2<MAP, INCL, PL_HIT, 0>(P, s);
+    if (pl == PL_TDUMP) return go2<MAP, INCL, PL_TDUMP, 0>(P, s);
+    if (pl == PL_EMPTY) return go2<MAP, INCL, PL_EMPTY, 0>(P, s);
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_thread2(const Params &P, bool lam, bool incl, int pl, int cs, cudaStream_t s)
+cudaError_t launch_thread2(const Params &P, int map, bool incl, int pl, int cs, cudaStream_t s)
 {
-    if (lam) return incl ? pick_pl<true, true>(P, pl, cs, s) : pick_pl<true, false>(P, pl, cs, s);
-    return incl ? pick_pl<false, true>(P, pl, cs, s) : pick_pl<false, false>(P, pl, cs, s);
+    if (map == SMAP_MAP_LAMBDA) return incl ? pick_pl<SMAP_MAP_LAMBDA, true>(P, pl, cs, s) : pick_pl<SMAP_MAP_LAMBDA, false>(P, pl, cs, s);
+    if (map == SMAP_MAP_ENUM) return incl ? pick_pl<SMAP_MAP_ENUM, true>(P, pl, cs, s) : pick_pl<SMAP_MAP_ENUM, false>(P, pl, cs, s);
+    return incl ? pick_pl<SMAP_MAP_BB, true>(P, pl, cs, s) : pick_pl<SMAP_MAP_BB, false>(P, pl, cs, s);
 }
 
 } // namespace smap

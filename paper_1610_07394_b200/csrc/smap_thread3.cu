@@ -7,12 +7,13 @@
 
 namespace smap {
 
-template <bool LAM, int PL, int CS>
+template <int MAP, int PL, int CS>
 __global__ void __launch_bounds__(512) k_thread3(Params P)
 {
+    constexpr bool LAM = MAP == SMAP_MAP_LAMBDA;
     const uint64_t bid = blockIdx.x;
     const uint32_t a = threadIdx.x, bb = threadIdx.y, c = threadIdx.z, rho = (uint32_t)P.rho;
-    const Blk3 B = LAM ? decode_lambda3(bid, P) : decode_bb3(bid, P);
+    const Blk3 B = decode3<MAP>(bid, P);
 
     if (PL == PL_MAPD) {
         if (a == 0 && bb == 0 && c == 0)
@@ -110,39 +111,41 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
     }
 }
 
-template <bool LAM, int PL, int CS>
+template <int MAP, int PL, int CS>
 static cudaError_t go3(const Params &P, cudaStream_t s)
 {
     dim3 block(P.rho, P.rho, P.rho);
-    k_thread3<LAM, PL, CS><<<(unsigned)P.nblocks, block, 0, s>>>(P);
+    k_thread3<MAP, PL, CS><<<(unsigned)P.nblocks, block, 0, s>>>(P);
     return cudaGetLastError();
 }
 
-template <bool LAM>
+template <int MAP>
 static cudaError_t pick3(const Params &P, int pl, int cs, cudaStream_t s)
 {
 #define CS3(PLV)                                          \
     if (pl == PLV) {                                      \
-        if (cs == 0) return go3<LAM, PLV, 0>(P, s);       \
-        if (cs == 1) return go3<LAM, PLV, 1>(P, s);       \
-        if (cs == 3) return go3<LAM, PLV, 3>(P, s);       \
-        return go3<LAM, PLV, 2>(P, s);                    \
+        if (cs == 0) return go3<MAP, PLV, 0>(P, s);       \
+        if (cs == 1) return go3<MAP, PLV, 1>(P, s);       \
+        if (cs == 3) return go3<MAP, PLV, 3>(P, s);       \
+        return go3<MAP, PLV, 2>(P, s);                    \
     }
     CS3(PL_IW32)
     CS3(PL_IW64)
 #undef CS3
-    if (pl == PL_ATM) return go3<LAM, PL_ATM, 0>(P, s);
-    if (pl == PL_TC) return go3<LAM, PL_TC, 0>(P, s);
-    if (pl == PL_MAPD) return go3<LAM, PL_MAPD, 0>(P, s);
-    if (pl == PL_HIT) return go3<LAM, PL_HIT, 0>(P, s);
-    if (pl == PL_TDUMP) return go3<LAM, PL_TDUMP, 0>(P, s);
-    if (pl == PL_EMPTY) return go3<LAM, PL_EMPTY, 0>(P, s);
+    if (pl == PL_ATM) return go3<MAP, PL_ATM, 0>(P, s);
+    if (pl == PL_TC) return go3<MAP, PL_TC, 0>(P, s);
+    if (pl == PL_MAPD) return go3<MAP, PL_MAPD, 0>(P, s);
+    if (pl == PL_HIT) return go3<MAP, PL_HIT, 0>(P, s);
+    if (pl == PL_TDUMP) return go3<MAP, PL_TDUMP, 0>(P, s);
+    if (pl == PL_EMPTY) return go3<MAP, PL_EMPTY, 0>(P, s);
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_thread3(const Params &P, bool lam, int pl, int cs, cudaStream_t s)
+cudaError_t launch_thread3(const Params &P, int map, int pl, int cs, cudaStream_t s)
 {
-    return lam ? pick3<true>(P, pl, cs, s) : pick3<false>(P, pl, cs, s);
+    if (map == SMAP_MAP_LAMBDA) return pick3<SMAP_MAP_LAMBDA>(P, pl, cs, s);
+    if (map == SMAP_MAP_ENUM) return pick3<SMAP_MAP_ENUM>(P, pl, cs, s);
+    return pick3<SMAP_MAP_BB>(P, pl, cs, s);
 }
 
 } // namespace smap

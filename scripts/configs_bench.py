@@ -1,5 +1,6 @@
 """Device-time table of every BASELINE.json config (C1..C5): lambda vs BB at the
-paper's one-element-per-thread granularity and at tile granularity.
+paper's one-element-per-thread granularity and at tile granularity, plus the
+root-based enumeration map (SMAP_MAP_ENUM) at thread granularity.
 CUDA events on the launching stream, warm-up, median of reps.  Writes
 gpurun_out/configs.json (copied into profiles/ per round).
 
@@ -37,16 +38,16 @@ def compare(m, n, payload, variants, pts=None, param=0.0, out=None, reps=10, dia
     rows = []
     for name, cfg in variants:
         res = {"variant": name, "cfg": cfg}
-        for mp in ("lambda", "bb"):
+        maps = ("lambda", "bb") + (("enum",) if cfg.get("granularity") == "thread" else ())
+        for mp in maps:
             c = dict(cfg)
             flags = c.pop("flags", 0)
-            if mp == "bb":
+            if mp != "lambda":
                 c.pop("order", None)
             plan = sm.smap_plan(m, n, map=mp, diag=diag, **c)
             q = sm.smap_plan_query(plan)
             ms = time_run(plan, payload, pts=pts, param=param, out=out, reps=reps, flags=flags)
             res[mp] = {"ms": round(ms, 4), "launched": q["launched_threads"], "blocks": q["grid_blocks"]}
-            e = sm.smap_run(plan, "empty") if False else None  # noqa: F841
             ems = time_run(plan, "empty", reps=reps)
             res[mp]["empty_ms"] = round(ems, 4)
             del plan
@@ -55,6 +56,8 @@ def compare(m, n, payload, variants, pts=None, param=0.0, out=None, reps=10, dia
         res["lambda_elems_per_s"] = V / (res["lambda"]["ms"] * 1e-3)
         res["speedup_lambda_vs_bb"] = round(res["bb"]["ms"] / res["lambda"]["ms"], 3)
         res["launch_ratio_bb_over_lambda"] = round(res["bb"]["launched"] / res["lambda"]["launched"], 4)
+        if "enum" in res:       # root-based enumeration map: same payload, fewer blocks than lambda3
+            res["speedup_lambda_vs_enum"] = round(res["enum"]["ms"] / res["lambda"]["ms"], 3)
         print(json.dumps(res), flush=True)
         rows.append(res)
     return rows
