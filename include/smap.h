@@ -61,7 +61,10 @@ typedef enum {
 
 typedef enum {
     SMAP_DIAG_STRICT = 0,    /* j < i  /  i < j < k */
-    SMAP_DIAG_INCLUSIVE = 1  /* j <= i (the paper's Delta_n^2); m=2 only */
+    SMAP_DIAG_INCLUSIVE = 1  /* j <= i (the paper's Delta_n^2) / i <= j <= k (Delta_n^3,
+                                P:559-563).  m=3 runs the strict set of n + 2 through the
+                                rank-preserving bijection (i, j, k) -> (i, j+1, k+2) (reading E24);
+                                no ATM / TC (defined on distinct triples) */
 } smap_diag;
 
 typedef enum {
@@ -98,7 +101,10 @@ typedef struct smap_plan_s *smap_plan_t;
 
 typedef struct {
     int     m;            /* 2 or 3 */
-    int64_t n;            /* elements per side; power of two */
+    int64_t n;            /* elements per side, any n in [m, 2^30]: the grid is built for
+                             n' = 2^ceil(log2 n) and elements with an index >= n are filtered
+                             ("approach n from above"); n' != n needs shard_count 1
+                             and the canonical layout */
     int     rho;          /* block side (threads per axis for THREAD, elements per axis for TILE); power of two */
     int     map;          /* smap_map */
     int     diag;         /* smap_diag */
@@ -149,10 +155,12 @@ typedef struct {
 
 /* Validate `d`, derive the grid and the closed forms, and allocate the plan's
  * scratch on d->device.  Host math plus small cudaMalloc's; launches nothing.
- * SMAP_E_INVALID: m not in {2,3}; n or rho not a power of two; N = n/rho too
- * small (m=2: N >= 2; m=3 lambda: N >= 8, BB: N >= 1); rho outside the
- * granularity's range; inclusive with m=3; shard_count not a power of two or
- * not dividing N/2, or > 1 with BB; persistent with THREAD granularity. */
+ * SMAP_E_INVALID: m not in {2,3}; n outside [m, 2^30]; rho not a power of two;
+ * N = n'/rho too small (m=2: N >= 2; m=3 lambda: N >= 8, BB: N >= 1), with
+ * n' = 2^ceil(log2 n) (2^ceil(log2 (n+2)) for m=3 inclusive); rho outside the
+ * granularity's range; shard_count not a power of two or not dividing N/2, or
+ * > 1 with BB / ENUM; persistent with THREAD granularity.
+ * SMAP_E_UNSUPPORTED: n' != n with shard_count > 1 or the tile-blocked layout. */
 smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out);
 
 /* Fill the closed-form fields of *st (others zero).  Host only. */

@@ -57,10 +57,12 @@ _SIGS = {
     "or_rank2_strict": (u64, [u64, u64]),
     "or_rank2_incl": (u64, [u64, u64]),
     "or_rank3": (u64, [u64, u64, u64]),
+    "or_rank3_incl": (u64, [u64, u64, u64]),
     "or_domain_volume": (u64, [i32, i32, u64]),
     "or_thread_elem2": (i32, [i32, i32, u64, u64, u64, u64, u64, u64, P]),
     "or_thread_elem3": (i32, [i32, u64, u64, u64, u64, u64, u64, u64, u64, P]),
     "or_grid_blocks": (u64, [i32, i32, i32, u64, u64]),
+    "or_padded_n": (u64, [u64]),
     "or_thread_dump": (i32, [i32, i32, i32, u64, u64, u64, u64, i32, P, u64]),
     "or_element_hits": (i32, [i32, i32, i32, u64, u64, u64, u64, i32, P, u64, P]),
     "or_column_work": (i64, [i32, i32, u64, u64, u64]),
@@ -167,6 +169,7 @@ def check_rec3(N): return lib().or_check_rec3(N)
 def rank2_strict(i, j): return lib().or_rank2_strict(i, j)
 def rank2_incl(i, j): return lib().or_rank2_incl(i, j)
 def rank3(i, j, k): return lib().or_rank3(i, j, k)
+def rank3_incl(i, j, k): return lib().or_rank3_incl(i, j, k)
 
 
 def _mapc(bb) -> int:
@@ -195,8 +198,13 @@ def grid_blocks(m, inclusive, bb, N, G=1):
 ORDERS = {"rows": 0, "squares": 1}
 
 
+def padded_n(n) -> int:
+    """n' = 2^ceil(log2 n), the grid size of "approach n from above"."""
+    return lib().or_padded_n(n)
+
+
 def thread_dump(m, inclusive, bb, n, rho, rank=0, G=1, order="rows") -> np.ndarray:
-    N = n // rho
+    N = padded_n(n) // rho
     length = grid_blocks(m, inclusive, bb, N, G) * rho ** m
     out = np.empty(length, np.uint64)
     assert lib().or_thread_dump(m, int(inclusive), _mapc(bb), n, rho, rank, G, ORDERS[order],

@@ -374,12 +374,19 @@ uint64_t or_rank3(uint64_t i, uint64_t j, uint64_t k)
     u128 ck3 = (u128)k * (k - 1) * (k - 2) / 6;
     return (uint64_t)ck3 + j * (j - 1) / 2 + i;
 }
+/* inclusive triples i <= j <= k in nested-loop order (k outer, i inner):
+ * C(k+2,3) + C(j+1,2) + i  (the paper's Delta_n^3 in the cell convention, E1) */
+uint64_t or_rank3_incl(uint64_t i, uint64_t j, uint64_t k)
+{
+    u128 t = (u128)k * (k + 1) * (k + 2) / 6;
+    return (uint64_t)t + j * (j + 1) / 2 + i;
+}
 
 /* Useful-element count V of each domain (closed forms of L0). */
 uint64_t or_domain_volume(int m, int inclusive, uint64_t n)
 {
     if (m == 2) return inclusive ? or_simplex_volume(2, n) : or_simplex_volume(2, n - 1);
-    if (m == 3) return n >= 2 ? or_simplex_volume(3, n - 2) : 0;
+    if (m == 3) return inclusive ? or_simplex_volume(3, n) : (n >= 2 ? or_simplex_volume(3, n - 2) : 0);
     return 0;
 }
 
@@ -463,6 +470,11 @@ int or_thread_elem3(int map, uint64_t N, uint64_t rho, uint64_t wx, uint64_t wy,
  * are t = ty*rho + tx (m=2) and t = (c*rho + b)*rho + a (m=3). */
 static uint64_t or_ipow(uint64_t b, int e) { uint64_t r = 1; while (e-- > 0) r *= b; return r; }
 
+/* "Approach n from above": for any n the grid is the one of
+ * n' = 2^ceil(log2 n), and threads whose element has an index >= n (the
+ * largest index: i for pairs j < i, k for triples i < j < k) are idle. */
+uint64_t or_padded_n(uint64_t n) { uint64_t p = 1; while (p < n) p *= 2; return p; }
+
 uint64_t or_grid_blocks(int m, int inclusive, int map, uint64_t N, uint64_t G)
 {
     if (map == 0) return or_ipow(N, m);
@@ -519,7 +531,9 @@ static int or_block_coords(int m, int inclusive, int map, uint64_t N, uint64_t r
 int or_thread_dump(int m, int inclusive, int map, uint64_t n, uint64_t rho, uint64_t rank,
                    uint64_t G, int order, uint64_t *out, uint64_t len)
 {
-    uint64_t N = n / rho, T = or_ipow(rho, m);
+    /* m=3 inclusive (reading E24): the strict map of n + 2, element (i, j, k) = (i', j'-1, k'-2) */
+    uint64_t nint = (m == 3 && inclusive) ? n + 2 : n;
+    uint64_t N = or_padded_n(nint) / rho, T = or_ipow(rho, m);
     uint64_t nb = or_grid_blocks(m, inclusive, map, N, G);
     if (nb * T != len) return -1;
     for (uint64_t bid = 0; bid < nb; bid++) {
@@ -531,9 +545,11 @@ int or_thread_dump(int m, int inclusive, int map, uint64_t n, uint64_t rho, uint
             if (m == 2) ok = or_thread_elem2(inclusive, map, N, rho, w[0], w[1], t % rho, t / rho, e);
             else ok = or_thread_elem3(map, N, rho, w[0], w[1], w[2], t % rho, (t / rho) % rho, t / (rho * rho), e);
             uint64_t p = UINT64_MAX;
+            if (ok && e[m == 2 ? 0 : 2] >= (int64_t)nint) ok = 0;  /* padded grid: beyond n */
             if (ok) {
                 if (m == 2) p = inclusive ? or_rank2_incl((uint64_t)e[0], (uint64_t)e[1])
                                           : or_rank2_strict((uint64_t)e[0], (uint64_t)e[1]);
+                else if (inclusive) p = or_rank3_incl((uint64_t)e[0], (uint64_t)e[1] - 1, (uint64_t)e[2] - 2);
                 else p = or_rank3((uint64_t)e[0], (uint64_t)e[1], (uint64_t)e[2]);
             }
             out[bid * T + t] = p;
@@ -548,7 +564,8 @@ int or_thread_dump(int m, int inclusive, int map, uint64_t n, uint64_t rho, uint
 int or_element_hits(int m, int inclusive, int map, uint64_t n, uint64_t rho, uint64_t rank,
                     uint64_t G, int order, uint32_t *hits, uint64_t V, int64_t *res)
 {
-    uint64_t N = n / rho, T = or_ipow(rho, m);
+    uint64_t nint = (m == 3 && inclusive) ? n + 2 : n;     /* E24 */
+    uint64_t N = or_padded_n(nint) / rho, T = or_ipow(rho, m);
     uint64_t nb = or_grid_blocks(m, inclusive, map, N, G);
     int64_t useful = 0, outside = 0;
     for (uint64_t bid = 0; bid < nb; bid++) {
@@ -560,14 +577,21 @@ int or_element_hits(int m, int inclusive, int map, uint64_t n, uint64_t rho, uin
             if (m == 2) ok = or_thread_elem2(inclusive, map, N, rho, w[0], w[1], t % rho, t / rho, e);
             else ok = or_thread_elem3(map, N, rho, w[0], w[1], w[2], t % rho, (t / rho) % rho, t / (rho * rho), e);
             if (!ok) continue;
+            if (e[m == 2 ? 0 : 2] >= (int64_t)nint && e[m == 2 ? 0 : 2] < (int64_t)(N * rho)) continue;  /* padded: idle */
+            if (m == 3 && inclusive) { e[1] -= 1; e[2] -= 2; }  /* E24: back to i <= j <= k */
             int in;
             uint64_t p;
             if (m == 2) {
                 in = e[1] >= 0 && e[0] < (int64_t)n && (inclusive ? e[1] <= e[0] : e[1] < e[0]);
                 p = in ? (inclusive ? or_rank2_incl(e[0], e[1]) : or_rank2_strict(e[0], e[1])) : 0;
             } else {
-                in = e[0] >= 0 && e[0] < e[1] && e[1] < e[2] && e[2] < (int64_t)n;
-                p = in ? or_rank3(e[0], e[1], e[2]) : 0;
+                if (inclusive) {
+                    in = e[0] >= 0 && e[0] <= e[1] && e[1] <= e[2] && e[2] < (int64_t)n;
+                    p = in ? or_rank3_incl(e[0], e[1], e[2]) : 0;
+                } else {
+                    in = e[0] >= 0 && e[0] < e[1] && e[1] < e[2] && e[2] < (int64_t)n;
+                    p = in ? or_rank3(e[0], e[1], e[2]) : 0;
+                }
             }
             if (!in || p >= V) { outside++; continue; }
             hits[p]++;
@@ -620,8 +644,8 @@ int or_index_write(int m, int inclusive, uint64_t n, void *out, int elem_bytes)
             }
     } else {
         for (uint64_t k = 0; k < n; k++)
-            for (uint64_t j = 0; j < k; j++)
-                for (uint64_t i = 0; i < j; i++) {
+            for (uint64_t j = 0; inclusive ? j <= k : j < k; j++)
+                for (uint64_t i = 0; inclusive ? i <= j : i < j; i++) {
                     if (elem_bytes == 4) o4[pos] = (uint32_t)pos; else o8[pos] = pos;
                     pos++;
                 }
@@ -803,9 +827,9 @@ int or_cs_index(int m, int inclusive, uint64_t n, uint64_t lo, uint64_t hi, int 
             uint64_t pos = inclusive ? or_rank2_incl(r, 0) : or_rank2_strict(r, 0);
             for (uint64_t j = 0; inclusive ? j <= r : j < r; j++, pos++) or_cs_add(c, pos, pos);
         } else {
-            for (uint64_t j = 0; j < r; j++) {
-                uint64_t pos = or_rank3(0, j, r);
-                for (uint64_t i = 0; i < j; i++, pos++) or_cs_add(c, pos, pos);
+            for (uint64_t j = 0; inclusive ? j <= r : j < r; j++) {
+                uint64_t pos = inclusive ? or_rank3_incl(0, j, r) : or_rank3(0, j, r);
+                for (uint64_t i = 0; inclusive ? i <= j : i < j; i++, pos++) or_cs_add(c, pos, pos);
             }
         }
         c0 += c[0]; c1 += c[1]; c2 += c[2]; c3 += c[3]; c4 ^= c[4];

@@ -76,6 +76,7 @@ uint64_t smap_volume(int m, int64_t n, int diag)
     if (n <= 0) return 0;
     unsigned __int128 N = (unsigned __int128)n;
     if (m == 2) return (uint64_t)(diag == SMAP_DIAG_INCLUSIVE ? N * (N + 1) / 2 : N * (N - 1) / 2);
+    if (m == 3 && diag == SMAP_DIAG_INCLUSIVE) return (uint64_t)(N * (N + 1) * (N + 2) / 6);
     if (m == 3) return n < 3 ? 0 : (uint64_t)(N * (N - 1) * (N - 2) / 6);
     return 0;
 }
@@ -100,9 +101,17 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (d->diag != SMAP_DIAG_STRICT && d->diag != SMAP_DIAG_INCLUSIVE) return fail(SMAP_E_INVALID, "bad diag %d", d->diag);
     if (d->granularity != SMAP_GRAN_THREAD && d->granularity != SMAP_GRAN_TILE)
         return fail(SMAP_E_INVALID, "bad granularity %d", d->granularity);
-    if (incl && m != 2) return fail(SMAP_E_INVALID, "inclusive diagonal is m=2 only");
-    if (!is_pow2(n) || n < 2 || n > ((int64_t)1 << 30)) return fail(SMAP_E_INVALID, "n must be a power of two in [2, 2^30] (got %lld)", (long long)n);
-    if (!is_pow2(rho) || rho > n) return fail(SMAP_E_INVALID, "rho must be a power of two <= n (got %d)", rho);
+    if (n < (incl ? 1 : m) || n > ((int64_t)1 << 30)) return fail(SMAP_E_INVALID, "n must be in [m, 2^30] (got %lld)", (long long)n);
+    // m=3 inclusive (the paper's Delta_n^3, i <= j <= k < n) runs as the strict set of
+    // n + 2 through the bijection (i, j, k) -> (i, j + 1, k + 2), which preserves the
+    // packed rank: C(k+2,3) + C(j+1,2) + i (reading E24)
+    const int64_t nint = (m == 3 && incl) ? n + 2 : n;
+    // "approach n from above": the grid is built for n' = 2^ceil(log2 n) and
+    // the elements with an index >= n are filtered out in the kernels
+    int64_t npad = 1;
+    while (npad < nint) npad <<= 1;
+    const bool padded = npad != nint;
+    if (!is_pow2(rho) || rho > npad) return fail(SMAP_E_INVALID, "rho must be a power of two <= 2^ceil(log2 n) (got %d)", rho);
     if (!tile) {
         if ((m == 2 && rho > 32) || (m == 3 && rho > 8))
             return fail(SMAP_E_INVALID, "THREAD granularity needs rho^m <= 1024 (rho=%d, m=%d)", rho, m);
@@ -112,7 +121,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
         if (!ok) return fail(SMAP_E_INVALID, "TILE rho must be in %s (got %d)", m == 2 ? "{32,...,512}" : "{8,16,32}", rho);
         if (d->persistent < 0) return fail(SMAP_E_INVALID, "persistent must be >= 0");
     }
-    const int64_t N = n / rho;
+    const int64_t N = npad / rho;
     if (m == 2 && lam && N < 2) return fail(SMAP_E_INVALID, "lambda2 needs N = n/rho >= 2");
     if (m == 3 && lam && N < 8) return fail(SMAP_E_INVALID, "lambda3 needs N = n/rho >= 8 (body blocks, E14)");
     if (G < 1 || !is_pow2(G)) return fail(SMAP_E_INVALID, "shard_count must be a power of two >= 1");
@@ -123,13 +132,15 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (d->layout != SMAP_LAYOUT_ROWS && d->layout != SMAP_LAYOUT_TILES) return fail(SMAP_E_INVALID, "bad layout %d", d->layout);
     if (d->layout == SMAP_LAYOUT_TILES && (m != 2 || !tile))
         return fail(SMAP_E_INVALID, "the tile-blocked layout is for m=2 TILE plans");
+    if (padded && G != 1) return fail(SMAP_E_UNSUPPORTED, "sharding needs n to be a power of two (padded grids are not volume-balanced)");
+    if (padded && d->layout == SMAP_LAYOUT_TILES) return fail(SMAP_E_UNSUPPORTED, "the tile-blocked layout needs n to be a power of two");
 
     smap_plan_s *p = new (std::nothrow) smap_plan_s();
     if (!p) return fail(SMAP_E_NOMEM, "host allocation failed");
     p->d = *d;
     Params &P = p->P;
     memset(&P, 0, sizeof P);
-    P.n = (int)n; P.N = (int)N; P.log2N = ilog2(N); P.rho = rho; P.log2rho = ilog2(rho);
+    P.n = (int)nint; P.N = (int)N; P.log2N = ilog2(N); P.rho = rho; P.log2rho = ilog2(rho);
     P.layout = d->layout;
     if (lam) {
         P.W = (int)(N / 2 / G); P.log2W = ilog2(P.W); P.wx0 = d->shard_rank * P.W;
@@ -246,6 +257,8 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     if (ipl == PL_EDM && (d.m != 2 || incl)) return fail(SMAP_E_INVALID, "EDM is defined on the m=2 strict domain");
     if ((ipl == PL_ATM || ipl == PL_TC) && d.m != 3) return fail(SMAP_E_INVALID, "ATM/TC are m=3 payloads");
     if ((ipl == PL_EDM || ipl == PL_ATM || ipl == PL_TC) && !points) return fail(SMAP_E_INVALID, "payload needs points");
+    if ((ipl == PL_ATM || ipl == PL_TC) && d.diag == SMAP_DIAG_INCLUSIVE)
+        return fail(SMAP_E_UNSUPPORTED, "ATM / TC are defined on distinct triples (strict diagonal)");
     if (ipl == PL_TDUMP && tile) return fail(SMAP_E_INVALID, "THREAD_DUMP needs THREAD granularity");
     size_t need = 0;
     smap_out_bytes(p, pl, &need);
@@ -265,8 +278,9 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     CK(cudaGetDevice(&cur));
     if (cur != p->device) CK(cudaSetDevice(p->device));
     const bool tc_bits = ipl == PL_TC && tile;
-    if (tc_bits && (d.n % 32) != 0) return fail(SMAP_E_UNSUPPORTED, "bit-sliced TC needs n to be a multiple of 32");
-    if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)d.n * (size_t)(d.n / 32) * sizeof(uint32_t)));
+    const int64_t npad = (int64_t)p->P.N * d.rho;          // bitmap over the padded index range
+    if (tc_bits && (npad % 32) != 0) return fail(SMAP_E_UNSUPPORTED, "bit-sliced TC needs 2^ceil(log2 n) >= 32");
+    if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)npad * (size_t)(npad / 32) * sizeof(uint32_t)));
     if (ipl == PL_ATM) {
         const uint64_t np = tile ? p->ctas : p->P.nblocks;
         if (np > p->npartials) {
@@ -288,7 +302,7 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     CK(cudaEventRecord(p->ev0, s));
     cudaError_t e;
     if (tc_bits) {
-        cudaError_t ea = launch_tc_adjacency(points, (int)d.n, param, p->d_adj, s);
+        cudaError_t ea = launch_tc_adjacency(points, (int)d.n, (int)npad, param, p->d_adj, s);
         if (ea != cudaSuccess) return cuda_fail(ea, "TC adjacency launch");
         launches++;
     }
@@ -345,9 +359,11 @@ smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *p
     const bool lam = d.map == SMAP_MAP_LAMBDA, incl = d.diag == SMAP_DIAG_INCLUSIVE;
     const int64_t n = d.n;
     if (d.m == 3) {
-        const int64_t i = e[0], j = e[1], k = e[2];
-        if (!(0 <= i && i < j && j < k && k < n)) return fail(SMAP_E_INVALID, "element outside the domain");
+        int64_t i = e[0], j = e[1], k = e[2];
+        if (incl ? !(0 <= i && i <= j && j <= k && k < n) : !(0 <= i && i < j && j < k && k < n))
+            return fail(SMAP_E_INVALID, "element outside the domain");
         if (lam && d.shard_count > 1) return fail(SMAP_E_UNSUPPORTED, "m=3 owner shard lookup is not implemented");
+        if (incl) { j += 1; k += 2; }                                  // E24 shift to the strict set of n + 2
         *shard = 0;
         *pos = (uint64_t)((unsigned __int128)k * (k - 1) * (k - 2) / 6) + (uint64_t)(j * (j - 1) / 2) + (uint64_t)i;
         return SMAP_OK;
@@ -415,7 +431,7 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
     cudaStream_t s = (cudaStream_t)stream;
     const float *dev_pts = nullptr;
     if (host_points) {
-        const size_t bytes = (size_t)p->P.n * 3 * sizeof(float);
+        const size_t bytes = (size_t)p->d.n * 3 * sizeof(float);
         if (!p->d_stage) CK(cudaMalloc(&p->d_stage, bytes));
         CK(cudaMemcpyAsync(p->d_stage, host_points, bytes, cudaMemcpyHostToDevice, s));
         dev_pts = p->d_stage;

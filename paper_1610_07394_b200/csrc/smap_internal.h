@@ -20,7 +20,7 @@ struct Result {
 enum Pl { PL_IW32 = 0, PL_IW64, PL_EDM, PL_ATM, PL_TC, PL_MAPD, PL_HIT, PL_TDUMP, PL_EMPTY };
 
 struct Params {
-    int n;          // elements per side
+    int n;          // elements per side (any n; the grid covers N * rho >= n)
     int N;          // blocks (tiles) per side = n / rho
     int log2N;
     int rho;        // block side (THREAD) or tile side (TILE)
@@ -45,9 +45,10 @@ cudaError_t launch_thread2(const Params &P, int map, bool incl, int pl, int cs, 
 cudaError_t launch_thread3(const Params &P, int map, int pl, int cs, cudaStream_t s);
 cudaError_t launch_tile2(const Params &P, int T, bool lam, bool incl, int pl, int cs, unsigned ctas, cudaStream_t s);
 cudaError_t launch_tile3(const Params &P, int T, bool lam, int pl, int cs, unsigned ctas, cudaStream_t s);
-// TC pre-pass: adj[j * (n/32) + w] bit b <=> r2(32w + b, j) < R*R (the same fp32
-// predicate as the per-triple compare); n a multiple of 32.
-cudaError_t launch_tc_adjacency(const float *pts, int n, float R, uint32_t *adj, cudaStream_t s);
+// TC pre-pass: adj[j * (npad/32) + w] bit b <=> 32w + b < n, j < n and
+// r2(32w + b, j) < R*R (the same fp32 predicate as the per-triple compare);
+// npad = N * rho, a multiple of 32.
+cudaError_t launch_tc_adjacency(const float *pts, int n, int npad, float R, uint32_t *adj, cudaStream_t s);
 // Deterministic fixed-order fp64 reduction of partials[0..np) into res->sum.
 // Adds the number of kernels it launched to *launches.
 cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res,

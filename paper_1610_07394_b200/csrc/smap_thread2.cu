@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(1024) k_thread2(Params P)
     } else {                              // inclusive diagonal block
         i = b.J * rho + ty; j = b.J * rho + tx; valid = tx <= ty; sj = 0;
     }
+    valid = valid && i < (uint32_t)P.n;     // padded grid: rows i >= n are filtered out
     const uint64_t p = INCL ? rank2i(i, j) : rank2s(i, j);
 
     (void)si; (void)li; (void)sj; (void)lj;   // (slot, local) coordinates: kept for staged variants

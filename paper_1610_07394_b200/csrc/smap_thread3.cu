@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
         else        { i = B.I * rho + c; j = B.K * rho + bb; k = B.K * rho + a; li = c; sj = 2; lk = a; }
         valid = a != bb;
     }
+    valid = valid && k < (uint32_t)P.n;     // padded grid: k >= n filtered out (k is the largest)
     const uint64_t p = valid ? rank3(i, j, k) : 0;
 
     if (PL == PL_TDUMP) {
@@ -78,7 +79,8 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
         if (tid < 3 * rho) {
             const uint32_t s = tid / rho, e = tid - s * rho;
             const uint32_t g = (s == 0 ? B.I : s == 1 ? B.J : B.K) * rho + e;
-            sp[tid] = make_float4(__ldg(P.pts + 3 * g), __ldg(P.pts + 3 * g + 1), __ldg(P.pts + 3 * g + 2), 0.f);
+            sp[tid] = g < (uint32_t)P.n ? make_float4(__ldg(P.pts + 3 * g), __ldg(P.pts + 3 * g + 1), __ldg(P.pts + 3 * g + 2), 0.f)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);   // padded index: never used
         }
         __syncthreads();
         const float4 pi = sp[si * rho + li], pj = sp[sj * rho + lj], pk = sp[sk * rho + lk];
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
         uint32_t cnt;
         if (LAM) cnt = B.cls == 2 ? body : (B.I < B.J ? r3 : face);
         else cnt = B.cls == 0 ? r3 : (B.cls == 2 ? body : face / 2);
+        if ((B.K + 1) * rho > (uint32_t)P.n) cnt = __syncthreads_count(valid);   // block cut by n (block-uniform)
         if (PL == PL_ATM) {
             const double t = valid ? (double)atm_term(rij, rjk, rik, P.param) : 0.0;
             const double s = block_sum_f64(t);

@@ -42,8 +42,8 @@ def test_volume(sm):
     assert sm.smap_volume(3, 2048) == 1429559296
 
 
-@pytest.mark.parametrize("kw", [dict(m=4, n=64, rho=8), dict(m=2, n=100, rho=4), dict(m=2, n=64, rho=128),
-                                dict(m=3, n=64, rho=8, diag="inclusive"), dict(m=2, n=64, rho=8, shard_count=3),
+@pytest.mark.parametrize("kw", [dict(m=4, n=64, rho=8), dict(m=2, n=100, rho=3), dict(m=2, n=64, rho=128),
+                                dict(m=2, n=1, rho=1), dict(m=3, n=2, rho=1), dict(m=2, n=64, rho=8, shard_count=3),
                                 dict(m=2, n=1024, rho=16, granularity="tile"), dict(m=3, n=32, rho=8),
                                 dict(m=2, n=64, rho=8, map="bb", shard_count=2)])
 def test_invalid_plans_rejected_before_device_work(sm, kw):

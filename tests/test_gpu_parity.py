@@ -293,8 +293,8 @@ def test_smallest_grids(sm, orc):
 
 
 def test_invalid_arguments(sm):
-    bad = [dict(m=4, n=64, rho=8), dict(m=2, n=100, rho=4), dict(m=2, n=64, rho=64),
-           dict(m=3, n=32, rho=8), dict(m=3, n=64, rho=8, diag="inclusive"), dict(m=2, n=64, rho=8, shard_count=3),
+    bad = [dict(m=4, n=64, rho=8), dict(m=2, n=100, rho=3), dict(m=2, n=64, rho=128), dict(m=2, n=1, rho=1),
+           dict(m=3, n=32, rho=8), dict(m=3, n=2, rho=1), dict(m=2, n=64, rho=8, shard_count=3),
            dict(m=2, n=64, rho=8, shard_count=8), dict(m=2, n=64, rho=8, map="bb", shard_count=2),
            dict(m=2, n=1024, rho=16, granularity="tile"), dict(m=2, n=1024, rho=16, persistent=2)]
     for kw in bad:
