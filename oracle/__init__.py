@@ -80,6 +80,8 @@ _SIGS = {
     "or_map_dump": (i32, [i32, i32, i32, u64, u64, u64, i32, P, u64]),
     "or_tile_layout2": (i32, [u64, u64, i32, i32, u64, u64, P, u64]),
     "or_cs_tiles2": (i32, [i32, u64, u64, i32, i32, u64, u64, P, i32, P]),
+    "or_tile_layout3": (i32, [u64, u64, i32, u64, u64, P, u64]),
+    "or_cs_tiles3": (i32, [u64, u64, i32, u64, u64, i32, P]),
 }
 
 
@@ -243,6 +245,30 @@ def cs_tiles2(payload, n, T, inclusive=False, bb=False, rank=0, G=1, points=None
     pp = _ptr(_pts(points)) if points is not None else None
     assert lib().or_cs_tiles2({"index_write": 0, "edm": 1}[payload], n, T, int(inclusive), _mapc(bb),
                               rank, G, pp, nthreads, _ptr(cs)) == 0
+    return dict(zip(CS_KEYS, (int(v) for v in cs)))
+
+
+def tile_layout3(n, T, bb=False, rank=0, G=1) -> np.ndarray:
+    """pos_of_rank[p] for the m=3 tile-blocked layout (or_tile_layout3, reading E26); -1 = other shard."""
+    V = domain_volume(3, False, n)
+    out = np.empty(V, np.int64)
+    assert lib().or_tile_layout3(n, T, _mapc(bb), rank, G, _ptr(out), V) == 0
+    return out
+
+
+def to_tile_layout3(canonical: np.ndarray, n, T, bb=False, rank=0, G=1) -> np.ndarray:
+    """Permute a canonical packed triple array into shard `rank`'s tile-blocked array."""
+    pos = tile_layout3(n, T, bb, rank, G)
+    own = pos >= 0
+    out = np.empty(int(own.sum()), canonical.dtype)
+    out[pos[own]] = canonical[own]
+    return out
+
+
+def cs_tiles3(n, T, bb=False, rank=0, G=1, nthreads=0):
+    """Streaming checksum of the m=3 index write in the tile-blocked layout."""
+    cs = np.zeros(5, np.uint64)
+    assert lib().or_cs_tiles3(n, T, _mapc(bb), rank, G, nthreads, _ptr(cs)) == 0
     return dict(zip(CS_KEYS, (int(v) for v in cs)))
 
 

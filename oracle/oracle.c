@@ -966,6 +966,124 @@ int or_cs_tiles2(int payload, uint64_t n, uint64_t T, int inclusive, int map, ui
 }
 
 /* ======================================================================
+ * m=3 tile-blocked layout (reading E26, the 3-D analogue of E23): every
+ * T^3 tile is one contiguous slot, slots in the launch order of the tile
+ * grid (lambda3 row order bid = (wz*N/2 + wy)*W + wx - wx0 within a shard;
+ * BB colex over the tiles I <= J <= K); idle tiles have no slot.  Inside a
+ * slot the elements follow the kernel's rows (k_l outer, j_l, i_l inner):
+ *   interior I<J<K:          all (i_l, j_l, k_l)
+ *   {I=J<K} segment:         i_l < j_l            (block triple (I, I, K))
+ *   {I<J=K} segment:         j_l < k_l            (block triple (I, K, K))
+ *   body I=J=K:              i_l < j_l < k_l
+ * A lambda face tile (I=J<K) holds the {I=J<K} segment followed by the
+ * {I<J=K} segment of (I, K) (reading E14); a BB tile holds its own class.
+ * Defined here by enumeration, in the plain order above.
+ * ====================================================================== */
+typedef struct { uint64_t I, J, K; int kind; } or_seg3;   /* kind 0 interior, 1 {I=J<K}, 2 {I<J=K}, 3 body */
+
+/* segments of the tile at launch position bid (returns the count, 0 = idle) */
+static int or_tile3_segments(int map, uint64_t N, uint64_t rank, uint64_t G, uint64_t bid, or_seg3 *sg)
+{
+    if (map == 0) {                               /* BB: bid = (K*N + J)*N + I */
+        uint64_t I = bid % N, J = (bid / N) % N, K = bid / (N * N);
+        if (!(I <= J && J <= K)) return 0;
+        sg[0].I = I; sg[0].J = J; sg[0].K = K;
+        sg[0].kind = (I < J && J < K) ? 0 : (I == J && J < K) ? 1 : (I < J) ? 2 : 3;
+        return 1;
+    }
+    uint64_t W = N / 2 / G, wx = rank * W + bid % W, wy = (bid / W) % (N / 2), wz = bid / W / (N / 2);
+    int64_t o[6];
+    int c = or_lambda3(N, wx, wy, wz, o);
+    if (c == OR_L3_FILLER || (c == OR_L3_SPARE && o[0] < 0)) return 0;
+    if (c == OR_L3_SPARE) { sg[0].I = sg[0].J = sg[0].K = (uint64_t)o[0]; sg[0].kind = 3; return 1; }
+    uint64_t I = (uint64_t)o[3], J = (uint64_t)o[4], K = (uint64_t)o[5];
+    if (I < J) { sg[0].I = I; sg[0].J = J; sg[0].K = K; sg[0].kind = 0; return 1; }
+    sg[0].I = I; sg[0].J = I; sg[0].K = K; sg[0].kind = 1;
+    sg[1].I = I; sg[1].J = K; sg[1].K = K; sg[1].kind = 2;
+    return 2;
+}
+
+static uint64_t or_seg3_size(int kind, uint64_t T)
+{
+    switch (kind) {
+    case 0: return T * T * T;
+    case 1: case 2: return T * T * (T - 1) / 2;
+    default: return T * (T - 1) * (T - 2) / 6;
+    }
+}
+
+/* calls f(pos, rank) for every element of segment s, positions from *pos on */
+#define OR_SEG3_WALK(s, T, POS, BODY)                                                        \
+    for (uint64_t kl = 0; kl < (T); kl++)                                                    \
+        for (uint64_t jl = 0; jl < (T); jl++) {                                              \
+            if (((s).kind == 2 || (s).kind == 3) && jl >= kl) continue;                      \
+            for (uint64_t il = 0; il < (T); il++) {                                          \
+                if (((s).kind == 1 || (s).kind == 3) && il >= jl) continue;                  \
+                uint64_t i_ = (s).I * (T) + il, j_ = (s).J * (T) + jl, k_ = (s).K * (T) + kl; \
+                uint64_t rank_ = or_rank3(i_, j_, k_);                                       \
+                BODY;                                                                        \
+                (POS)++;                                                                     \
+            }                                                                                \
+        }
+
+static uint64_t or_tile3_grid(int map, uint64_t N, uint64_t G)
+{
+    return map == 0 ? N * N * N : (N / 2 / G) * (N / 2) * (3 * N / 4);
+}
+
+int or_tile_layout3(uint64_t n, uint64_t T, int map, uint64_t rank, uint64_t G, int64_t *pos_of_rank, uint64_t V)
+{
+    uint64_t N = n / T, nb = or_tile3_grid(map, N, G);
+    for (uint64_t p = 0; p < V; p++) pos_of_rank[p] = -1;
+    uint64_t pos = 0;
+    for (uint64_t bid = 0; bid < nb; bid++) {
+        or_seg3 sg[2];
+        int ns = or_tile3_segments(map, N, rank, G, bid, sg);
+        for (int t = 0; t < ns; t++) {
+            OR_SEG3_WALK(sg[t], T, pos, {
+                if (rank_ >= V) return -1;
+                pos_of_rank[rank_] = (int64_t)pos;
+            })
+        }
+    }
+    return 0;
+}
+
+/* Streaming checksum (E21) of the m=3 index write (value = canonical rank) in
+ * the E26 layout: the slot offsets are counted up front (plain sums of the
+ * segment sizes), then the tiles are walked in parallel. */
+int or_cs_tiles3(uint64_t n, uint64_t T, int map, uint64_t rank, uint64_t G, int nthreads, uint64_t *cs)
+{
+    uint64_t N = n / T, nb = or_tile3_grid(map, N, G);
+    uint64_t *off = malloc((nb + 1) * sizeof(uint64_t));
+    if (!off) return -1;
+    off[0] = 0;
+    for (uint64_t bid = 0; bid < nb; bid++) {
+        or_seg3 sg[2];
+        int ns = or_tile3_segments(map, N, rank, G, bid, sg);
+        uint64_t s = 0;
+        for (int t = 0; t < ns; t++) s += or_seg3_size(sg[t].kind, T);
+        off[bid + 1] = off[bid] + s;
+    }
+    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+    int nt = or_threads(nthreads);
+    #pragma omp parallel for schedule(dynamic, 4) reduction(+:c0,c1,c2,c3) reduction(^:c4) num_threads(nt)
+    for (uint64_t bid = 0; bid < nb; bid++) {
+        uint64_t c[5] = {0, 0, 0, 0, 0};
+        or_seg3 sg[2];
+        int ns = or_tile3_segments(map, N, rank, G, bid, sg);
+        uint64_t pos = off[bid];
+        for (int t = 0; t < ns; t++) {
+            OR_SEG3_WALK(sg[t], T, pos, { or_cs_add(c, pos, rank_); })
+        }
+        c0 += c[0]; c1 += c[1]; c2 += c[2]; c3 += c[3]; c4 ^= c[4];
+    }
+    free(off);
+    cs[0] = c0; cs[1] = c1; cs[2] = c2; cs[3] = c3; cs[4] = c4;
+    return 0;
+}
+
+/* ======================================================================
  * Expected MAP_DUMP records (format of include/smap.h, restated): per grid
  * block in launch order, int32 {x0, x1, x2, cls}.
  * ====================================================================== */

@@ -130,8 +130,10 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (d->shard_rank < 0 || d->shard_rank >= G) return fail(SMAP_E_INVALID, "shard_rank out of range");
     if (d->order != SMAP_ORDER_ROWS && d->order != SMAP_ORDER_SQUARES) return fail(SMAP_E_INVALID, "bad order %d", d->order);
     if (d->layout != SMAP_LAYOUT_ROWS && d->layout != SMAP_LAYOUT_TILES) return fail(SMAP_E_INVALID, "bad layout %d", d->layout);
-    if (d->layout == SMAP_LAYOUT_TILES && (m != 2 || !tile))
-        return fail(SMAP_E_INVALID, "the tile-blocked layout is for m=2 TILE plans");
+    if (d->layout == SMAP_LAYOUT_TILES && !tile)
+        return fail(SMAP_E_INVALID, "the tile-blocked layout is for TILE plans");
+    if (d->layout == SMAP_LAYOUT_TILES && m == 3 && incl)
+        return fail(SMAP_E_UNSUPPORTED, "the m=3 tile-blocked layout is for the strict diagonal");
     if (padded && G != 1) return fail(SMAP_E_UNSUPPORTED, "sharding needs n to be a power of two (padded grids are not volume-balanced)");
     if (padded && d->layout == SMAP_LAYOUT_TILES) return fail(SMAP_E_UNSUPPORTED, "the tile-blocked layout needs n to be a power of two");
 
@@ -362,10 +364,44 @@ smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *p
         int64_t i = e[0], j = e[1], k = e[2];
         if (incl ? !(0 <= i && i <= j && j <= k && k < n) : !(0 <= i && i < j && j < k && k < n))
             return fail(SMAP_E_INVALID, "element outside the domain");
-        if (lam && d.shard_count > 1) return fail(SMAP_E_UNSUPPORTED, "m=3 owner shard lookup is not implemented");
         if (incl) { j += 1; k += 2; }                                  // E24 shift to the strict set of n + 2
-        *shard = 0;
-        *pos = (uint64_t)((unsigned __int128)k * (k - 1) * (k - 2) / 6) + (uint64_t)(j * (j - 1) / 2) + (uint64_t)i;
+        const uint64_t canon = (uint64_t)((unsigned __int128)k * (k - 1) * (k - 2) / 6) + (uint64_t)(j * (j - 1) / 2) + (uint64_t)i;
+        if (!lam) {
+            *shard = 0;
+            *pos = d.layout == SMAP_LAYOUT_ROWS ? canon
+                 : tile_slot3_bb((uint64_t)i / d.rho, (uint64_t)j / d.rho, (uint64_t)k / d.rho, d.rho)
+                   + seg3_local(((i / d.rho == j / d.rho) && (j / d.rho == k / d.rho)) ? 3 : (i / d.rho == j / d.rho) ? 1
+                                : (j / d.rho == k / d.rho) ? 2 : 0, i % d.rho, j % d.rho, k % d.rho, d.rho);
+            return SMAP_OK;
+        }
+        // lambda3^-1 (reading R3 inverted): the tile holding (i, j, k) and its grid position
+        const uint64_t T = (uint64_t)d.rho, N = (uint64_t)p->P.N, h = N / 2, W = (uint64_t)p->P.W;
+        const uint64_t bi = (uint64_t)i / T, bj = (uint64_t)j / T, bk = (uint64_t)k / T;
+        const uint64_t il = (uint64_t)i % T, jl = (uint64_t)j % T, kl = (uint64_t)k % T;
+        uint64_t wx, wy, wz, half = 0;
+        int kind;
+        if (bi == bj && bj == bk) {                                    // body tile d in the spare row (E14)
+            kind = 3;
+            if (bi < h) { wx = bi; wy = 0; wz = h; } else { wx = bi - h; wy = 0; wz = h + 1; }
+        } else {
+            uint64_t I = bi, Kb = bk, Z;
+            if (bi == bj) { kind = 1; Z = 0; }                         // {I=J<K} half of face tile (I, I, K)
+            else if (bj == bk) { kind = 2; Z = 0; half = T * T * (T - 1) / 2; }   // {I<J=K} half of face tile (I, I, K)
+            else { kind = 0; Z = bj - bi; }
+            // (X, Y, Z) = (I, K, J - I): b = 2^floor(log2(X ^ Y)), q = X >> (log2 b + 1)
+            const int l = floor_log2_u64(I ^ Kb);
+            const uint64_t b = 1ull << l, q = I >> (l + 1);
+            const uint64_t u0 = I - 2 * q * b, v0 = Kb - 2 * q * b - b;
+            uint64_t u, v, w;
+            if (Z < b) { u = u0; v = v0; w = Z; }                      // inside branch
+            else { u = b - 1 - u0; v = b - 1 - v0; w = 2 * b - 1 - Z; } // reflected branch
+            if (b == h) { wx = u; wy = v; wz = w; }                    // main cube (level N/2, q = 0)
+            else { wx = q * b + u; wy = b + v; wz = h + w; }           // slab level b
+        }
+        const int owner = (int)(wx / W);
+        *shard = owner;
+        if (d.layout == SMAP_LAYOUT_ROWS) { *pos = canon; return SMAP_OK; }
+        *pos = tile_slot3_lambda(wx - (uint64_t)owner * W, wy, wz, W, h, T) + half + seg3_local(kind, il, jl, kl, T);
         return SMAP_OK;
     }
     const int64_t i = e[0], j = e[1];

@@ -39,6 +39,75 @@ struct Params {
     const uint32_t *adj;           // TC (TILE): pair-predicate bitmap, n rows of n/32 words
 };
 
+// ---------------------------------------------------------------- m=3 tile-blocked layout (E26)
+// Slot offsets (elements, shard-local) of a T^3 tile in the tile-blocked
+// layout: slots in launch order, sizes T^3 (interior), T^2(T-1) (lambda face
+// tile: {I=J<K} then {I<J=K}), T^2(T-1)/2 (BB face tiles), C(T,3) (body),
+// 0 (idle).  Shared by the kernels and smap_locate.
+struct Slot3Sizes {
+    uint64_t full, face, half, body;
+};
+__host__ __device__ __forceinline__ Slot3Sizes slot3_sizes(uint64_t T)
+{
+    Slot3Sizes s;
+    s.full = T * T * T;
+    s.half = T * T * (T - 1) / 2;
+    s.face = 2 * s.half;
+    s.body = T * (T - 1) * (T - 2) / 6;
+    return s;
+}
+
+// lambda3, row launch order: tile at grid position (wx, wy, wz), x = wx - wx0,
+// W columns per shard, h = N/2.  Main cube: layer wz = 0 is all face tiles,
+// layers 1..h-1 all full.  Slab layer w = wz - h: row 0 holds body tiles for
+// w <= 1 (idle otherwise); rows wy >= 1 are faces (w = 0), fillers
+// (w >= 2^floor(log2 wy)), or full tiles -- i.e. full for wy >= r0(w) =
+// 2^(floor(log2 w) + 1).
+__host__ __device__ __forceinline__ uint64_t tile_slot3_lambda(uint64_t x, uint64_t wy, uint64_t wz, uint64_t W,
+                                                                uint64_t h, uint64_t T)
+{
+    const Slot3Sizes z = slot3_sizes(T);
+    if (wz == 0) return (wy * W + x) * z.face;
+    if (wz < h) return h * W * z.face + ((wz - 1) * h * W + wy * W + x) * z.full;
+    const uint64_t w = wz - h;
+    uint64_t off = h * W * z.face + (h - 1) * h * W * z.full;         // the main cube
+    if (w >= 1) off += W * z.body + (h - 1) * W * z.face;             // slab layer 0
+    if (w >= 2) off += W * z.body + (h > 2 ? h - 2 : 0) * W * z.full; // slab layer 1 (full rows wy >= 2)
+    for (uint64_t e = 1; ((uint64_t)1 << e) < w; e++) {               // layers [2^e, 2^(e+1)) below w: rows wy >= 2^(e+1)
+        const uint64_t lo = (uint64_t)1 << e, hi = lo << 1;
+        const uint64_t cnt = (w < hi ? w : hi) - lo, rows = h > hi ? h - hi : 0;
+        off += cnt * rows * W * z.full;
+    }
+    if (wy == 0) return off + x * z.body;                             // body tile (w <= 1)
+    if (w <= 1) off += W * z.body;
+    if (w == 0) return off + ((wy - 1) * W + x) * z.face;
+    uint64_t r0 = 2;
+    while (r0 <= w) r0 <<= 1;                                         // 2^(floor(log2 w) + 1)
+    return off + ((wy - r0) * W + x) * z.full;
+}
+
+// BB: tiles I <= J <= K in colex order (K outer, I inner).
+__host__ __device__ __forceinline__ uint64_t tile_slot3_bb(uint64_t I, uint64_t J, uint64_t K, uint64_t T)
+{
+    const Slot3Sizes z = slot3_sizes(T);
+    const uint64_t c3 = K * (K - 1) * (K - 2) / 6, c2 = K * (K - 1) / 2;   // (K < 3 / K < 2 give 0)
+    const uint64_t base = (K >= 3 ? c3 : 0) * z.full + 2 * (K >= 2 ? c2 : 0) * z.half + K * z.body;
+    if (J < K) return base + (J * (J - 1) / 2) * z.full + J * z.half + I * z.full;
+    return base + c2 * z.full + K * z.half + I * z.half;
+}
+
+// position of element (il, jl, kl) inside a segment of kind 0 interior,
+// 1 {I=J<K} (il < jl), 2 {I<J=K} (jl < kl), 3 body (il < jl < kl)
+__host__ __device__ __forceinline__ uint64_t seg3_local(int kind, uint64_t il, uint64_t jl, uint64_t kl, uint64_t T)
+{
+    switch (kind) {
+    case 0: return (kl * T + jl) * T + il;
+    case 1: return kl * (T * (T - 1) / 2) + jl * (jl - 1) / 2 + il;
+    case 2: return (kl * (kl - 1) / 2 + jl) * T + il;
+    default: return kl * (kl - 1) * (kl - 2) / 6 + jl * (jl - 1) / 2 + il;
+    }
+}
+
 // Kernel launchers (one per translation unit).  Return cudaErrorInvalidValue
 // for a combination that has no instantiated kernel.
 cudaError_t launch_thread2(const Params &P, int map, bool incl, int pl, int cs, cudaStream_t s);

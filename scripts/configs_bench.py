@@ -99,7 +99,11 @@ def main():
         out = torch.empty(sm.smap_volume(3, n), dtype=torch.int32, device="cuda")
         var = [("thread_rho8", dict(rho=8, granularity="thread")), ("tile_rho16", dict(rho=16, granularity="tile")),
                ("tile_rho32", dict(rho=32, granularity="tile"))]
-        table["configs"]["C3_index_write"] = compare(3, n, "index_write", var, out=out, reps=a.reps)
+        table["configs"]["C3_index_write"] = compare(3, n, "index_write", var + [
+            ("tile_rho16_tiles", dict(rho=16, granularity="tile", layout="tiles")),
+            ("tile_rho32_tiles", dict(rho=32, granularity="tile", layout="tiles")),
+            ("tile_rho32_tiles_xor", dict(rho=32, granularity="tile", layout="tiles", flags=sm.RUN_XOR))],
+            out=out, reps=a.reps)
         table["configs"]["C3_atm"] = compare(3, n, "atm", var, pts=p, param=1e-2, reps=a.reps)
         del out
     if "C4" in only:

@@ -75,6 +75,31 @@ def test_c3_index_and_atm_full(sm, orc):
         assert abs(st["sum"] - ref) <= 1e-5 * abs(ref)
 
 
+def test_c3_index_write_tile_layout_full(sm, orc):
+    """C3 index write in the m=3 tile-blocked layout (reading E26): full-size
+    streaming checksums against the oracle's enumerated layout, unsharded and
+    as 4 shards, plus sampled positions through smap_locate."""
+    n = workloads.CONFIGS["C3"]["n"]
+    V = math.comb(n, 3)
+    for bb, G in ((False, 1), (False, 4), (True, 1)):
+        for r in range(G):
+            plan = sm.smap_plan(3, n, 32, map="bb" if bb else "lambda", granularity="tile", shard_rank=r,
+                                shard_count=G, layout="tiles")
+            out = sm.alloc_out(plan, "index_write")
+            sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM_MIX)
+            st = sm.smap_stats_fetch(plan)
+            cs = orc.cs_tiles3(n, 32, bb, r, G)
+            assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+            assert st["count"] * G == V if not bb else st["count"] == V
+            got = out.cpu().numpy().view(np.uint32)
+            rng = np.random.default_rng(r)
+            for _ in range(2000):
+                i, j, k = sorted(int(v) for v in rng.choice(n, 3, replace=False))
+                sh, pos = sm.smap_locate(plan, i, j, k)
+                if sh == r:
+                    assert got[pos] == math.comb(k, 3) + math.comb(j, 2) + i
+
+
 def test_c5_tc_full(sm, orc):
     c = workloads.CONFIGS["C5"]
     n = c["n"]
