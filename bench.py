@@ -136,6 +136,19 @@ def cpu_baseline(target_core_seconds=20.0):
             "seconds": dt}
 
 
+def bench_config(G):
+    """The `config` object of the bench line (both arms): the C2 workload and
+    the launch configuration our arm times."""
+    cfg = workloads.BENCH_EDM
+    return {"workload": "C2: m=2 EDM strict lower triangle, n=65536, d=3 fp32 (BASELINE configs[1])",
+            "map": "lambda2", "granularity": cfg["granularity"], "tile": cfg["rho"],
+            "order": cfg.get("order", "rows"), "persistent": cfg.get("persistent", 0),
+            "layout": ("lambda-order tile-blocked packed lower triangle (DESIGN E23)"
+                       if cfg.get("layout") == "tiles" else "canonical packed rows (DESIGN E16)"),
+            "elements": N_POINTS * (N_POINTS - 1) // 2, "parallelism": f"omega_x shards x{G}",
+            "l2": "output 8.59 GB per step >> 126 MB L2 (no flush needed; points stay L2-resident by design)"}
+
+
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
@@ -156,10 +169,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (uniform [0,1)^3 fp32 points, seed 161007394)",
-        "config": {"workload": "C2: m=2 EDM strict lower triangle, n=65536, d=3 fp32",
-                   "sample_rows": [lo, hi - 1], "pairs_per_step": pairs},
+        "config": bench_config(args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"rows {lo}..{hi - 1} ({pairs} pairs) per step, {cores} OpenMP threads"},
+                         "sample": f"oracle or_cs_edm (fp32 distances + streaming checksums) on rows {lo}..{hi - 1} "
+                                   f"of the same workload ({pairs} pairs) per step, {cores} OpenMP threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -382,13 +395,7 @@ def main():
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (uniform [0,1)^3 fp32 points, seed 161007394)",
-            "config": {"workload": "C2: m=2 EDM strict lower triangle, n=65536, d=3 fp32 (BASELINE configs[1])",
-                       "map": "lambda2", "granularity": cfg["granularity"], "tile": cfg["rho"],
-                       "order": cfg.get("order", "rows"), "persistent": cfg.get("persistent", 0),
-                       "layout": ("lambda-order tile-blocked packed lower triangle (DESIGN E23)"
-                                  if cfg.get("layout") == "tiles" else "canonical packed rows (DESIGN E16)"),
-                       "elements": V, "parallelism": f"omega_x shards x{G}",
-                       "l2": "output 8.59 GB per step >> 126 MB L2 (no flush needed; points stay L2-resident by design)"},
+            "config": bench_config(G),
             "e2e": {"value": V / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": n * 12,
                     "d2h_bytes_per_step": 56, "ms_per_step": e2e_ms},
             "gpu_launches": launches_per_step * args.steps,
