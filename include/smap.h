@@ -75,7 +75,8 @@ typedef enum {
     /* one rho^m TILE of elements per 256-thread CTA step: lambda is applied to
      * tiles (the same map, coarser blocks); threads loop over the tile rows
      * with lanes on the contiguous axis; diagonal tiles are clipped per row
-     * instead of folded.  m=2: rho in {32,64,128,256,512}; m=3: rho in {8,16,32}. */
+     * instead of folded.  m=2: rho in {32,64,128,256,512}; m=3: rho in {8,16,32,64}
+     * (ATM: rho <= 32). */
     SMAP_GRAN_TILE = 1
 } smap_granularity;
 

@@ -117,8 +117,8 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
             return fail(SMAP_E_INVALID, "THREAD granularity needs rho^m <= 1024 (rho=%d, m=%d)", rho, m);
         if (d->persistent) return fail(SMAP_E_INVALID, "persistent CTAs need TILE granularity");
     } else {
-        const bool ok = m == 2 ? (rho >= 32 && rho <= 512) : (rho == 8 || rho == 16 || rho == 32);
-        if (!ok) return fail(SMAP_E_INVALID, "TILE rho must be in %s (got %d)", m == 2 ? "{32,...,512}" : "{8,16,32}", rho);
+        const bool ok = m == 2 ? (rho >= 32 && rho <= 512) : (rho >= 8 && rho <= 64);
+        if (!ok) return fail(SMAP_E_INVALID, "TILE rho must be in %s (got %d)", m == 2 ? "{32,...,512}" : "{8,16,32,64}", rho);
         if (d->persistent < 0) return fail(SMAP_E_INVALID, "persistent must be >= 0");
     }
     const int64_t N = npad / rho;
@@ -259,6 +259,8 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     if (ipl == PL_EDM && (d.m != 2 || incl)) return fail(SMAP_E_INVALID, "EDM is defined on the m=2 strict domain");
     if ((ipl == PL_ATM || ipl == PL_TC) && d.m != 3) return fail(SMAP_E_INVALID, "ATM/TC are m=3 payloads");
     if ((ipl == PL_EDM || ipl == PL_ATM || ipl == PL_TC) && !points) return fail(SMAP_E_INVALID, "payload needs points");
+    if (ipl == PL_ATM && tile && d.m == 3 && d.rho > 32)
+        return fail(SMAP_E_UNSUPPORTED, "ATM tiles are rho <= 32 (three rho x rho r^2 tables in shared memory)");
     if ((ipl == PL_ATM || ipl == PL_TC) && d.diag == SMAP_DIAG_INCLUSIVE)
         return fail(SMAP_E_UNSUPPORTED, "ATM / TC are defined on distinct triples (strict diagonal)");
     if (ipl == PL_TDUMP && tile) return fail(SMAP_E_INVALID, "THREAD_DUMP needs THREAD granularity");

@@ -309,3 +309,33 @@ def test_invalid_arguments(sm):
         sm.smap_run(plan, "atm", out=None)        # m=3 payload on an m=2 plan
     with pytest.raises(sm.SmapError):
         sm.smap_run(plan, "edm", out=sm.alloc_out(plan, "edm"))   # no points
+
+
+# ---------------------------------------------------------------- m=3 tiles of 64 (TC / index write / cover)
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+def test_tile64_m3(sm, orc, map_):
+    """rho = 64 m=3 tiles (64-bit predicate rows for TC; two lane chunks per
+    row in the index walker): exact cover, index write in both layouts, TC
+    count against the oracle, the map dump; ATM is rejected (smem tables)."""
+    n = 512 if map_ == "lambda" else 256
+    plan = sm.smap_plan(3, n, 64, map=map_, granularity="tile")
+    out, _ = run(sm, plan, "hitcount", zero=True)
+    assert (out.cpu().numpy() == 1).all()
+    out, _ = run(sm, plan, "map_dump")
+    np.testing.assert_array_equal(out.cpu().numpy().reshape(-1, 4), orc.map_dump(3, False, map_ == "bb", n // 64))
+    iw = orc.index_write(3, False, n)
+    out, st = run(sm, plan, "index_write", flags=sm.RUN_CHECKSUM_MIX)
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), iw)
+    plan_t = sm.smap_plan(3, n, 64, map=map_, granularity="tile", layout="tiles")
+    out, st = run(sm, plan_t, "index_write", flags=sm.RUN_XOR)
+    exp = orc.to_tile_layout3(iw, n, 64, map_ == "bb")
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), exp)
+    cs = orc.cs_array(exp)
+    assert (st["count"], st["xr"]) == (cs["count"], cs["xr"])
+    p = workloads.points(n, workloads.SEED_C5)
+    for R in (0.5, 0.2, 10.0):
+        _, st = run(sm, plan, "tc", points=dev_points(p), param=R)
+        assert st["count"] == math.comb(n, 3)
+        assert st["tc"] == orc.tc_count(p, np.float32(R))
+    with pytest.raises(sm.SmapError):
+        sm.smap_run(plan, "atm", points=dev_points(p), param=1e-2)
