@@ -117,7 +117,12 @@ class Plan:
     def n(self): return self.desc.n
 
     def __del__(self):
-        smap_destroy(self)
+        # at interpreter shutdown the module globals may already be gone; the
+        # process exit releases the device memory then
+        try:
+            smap_destroy(self)
+        except (TypeError, AttributeError):
+            pass
 
 
 def smap_plan(m: int, n: int, rho: int, map: str = "lambda", diag: str = "strict", granularity: str = "thread",
