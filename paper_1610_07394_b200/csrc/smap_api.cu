@@ -163,6 +163,11 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     p->useful = lam ? p->V / (uint64_t)G : p->V;
     p->elem64 = p->V > ((uint64_t)1 << 32);
 
+    if (!tile && P.nblocks > 0x7fffffffull) {
+        delete p;
+        return fail(SMAP_E_INVALID, "grid of %llu blocks exceeds one launch; use TILE granularity",
+                    (unsigned long long)P.nblocks);
+    }
     int dev = d->device;
     if (dev == SMAP_DEVICE_NONE) {            // host-only plan: validation + closed forms, no device work
         p->device = dev;
@@ -185,10 +190,6 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
         if (want > P.nblocks) want = P.nblocks;
         if (want > 0x7fffffffull) { delete p; return fail(SMAP_E_INVALID, "too many tiles for one launch"); }
         p->ctas = (unsigned)want;
-    } else if (P.nblocks > 0x7fffffffull) {
-        delete p;
-        return fail(SMAP_E_INVALID, "grid of %llu blocks exceeds one launch; use TILE granularity",
-                    (unsigned long long)P.nblocks);
     }
     if ((e = cudaMalloc(&p->d_res, sizeof(Result))) != cudaSuccess ||
         (e = cudaMallocHost(&p->h_res, sizeof(Result))) != cudaSuccess ||

@@ -61,3 +61,29 @@ def test_package_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", "liboracle", "oracle.c", "or_lambda"):
                     assert bad not in src, (f, bad)
+
+
+def test_extreme_sizes_host_plans(sm):
+    """Largest and smallest domains: closed forms exact in 64 bits (Python ints
+    as the reference), u64 elements above 2^32, one-launch grid limits."""
+    import math
+    N = sm.DEVICE_NONE
+    n = 1 << 30
+    for diag, V in (("strict", math.comb(n, 2)), ("inclusive", n * (n + 1) // 2)):
+        assert sm.smap_volume(2, n, diag) == V
+        plan = sm.smap_plan(2, n, 512, diag=diag, granularity="tile", device=N, layout="tiles")
+        q = sm.smap_plan_query(plan)
+        assert q["useful_elems"] == V and q["launched_threads"] == q["grid_blocks"] * 512 ** 2
+        assert sm.smap_out_bytes(plan, "index_write") == 8 * V          # u64 ranks beyond 2^32
+        assert sm.smap_out_bytes(plan, "edm") == 4 * V
+    assert sm.smap_volume(3, 1 << 21) == math.comb(1 << 21, 3)
+    # a THREAD grid beyond one launch (2^31 - 1 blocks) is refused on the host
+    with pytest.raises(sm.SmapError) as e:
+        sm.smap_plan(2, 1 << 17, 2, map="bb", device=N)                  # 2^32 blocks
+    assert e.value.status == 1
+    sm.smap_plan(2, 1 << 16, 2, map="lambda", device=N)                  # 2^29 blocks: fine
+    # smallest domains: one pair, one triple, one inclusive triple
+    assert sm.smap_volume(2, 2) == 1 and sm.smap_volume(3, 3) == 1 and sm.smap_volume(3, 1, "inclusive") == 1
+    for m, n_, d in ((2, 2, "strict"), (3, 3, "strict"), (3, 1, "inclusive"), (2, 1, "inclusive")):
+        q = sm.smap_plan_query(sm.smap_plan(m, n_, 1, map="bb", diag=d, device=N))
+        assert q["useful_elems"] == sm.smap_volume(m, n_, d)
