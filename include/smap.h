@@ -88,15 +88,19 @@ typedef enum {
     SMAP_PAYLOAD_MAP_DUMP = 4,    /* int32[4] per grid block/tile in launch order (see below) */
     SMAP_PAYLOAD_HITCOUNT = 5,    /* uint32 out[p] += 1 per mapped element (caller zeroes out) */
     SMAP_PAYLOAD_THREAD_DUMP = 6, /* THREAD gran. only: uint64 per launched thread, p or UINT64_MAX */
-    SMAP_PAYLOAD_EMPTY = 7        /* decode only, no element work (block-scheduling microbenchmark) */
+    SMAP_PAYLOAD_EMPTY = 7,       /* decode only, no element work (block-scheduling microbenchmark) */
+    SMAP_PAYLOAD_INDEX_WRITE_ATM = 8 /* m=3 strict, one pass (config C3, "index-write plus triple-interaction
+                                        sum"): out[p] = p as INDEX_WRITE (same out buffer, layout, flags)
+                                        AND the ATM sum of the same triples as ATM (param = eps^2,
+                                        stats.sum); TILE rho <= 32 or THREAD */
 } smap_payload;
 
 #define SMAP_DEVICE_NONE (-2)      /* smap_plan_desc.device: host-only plan */
 
 /* smap_run flags */
-#define SMAP_RUN_CHECKSUM     0x1u /* INDEX_WRITE/EDM: accumulate s0, s1 (E21) */
-#define SMAP_RUN_CHECKSUM_MIX 0x2u /* INDEX_WRITE/EDM: also accumulate mix (E21); implies CHECKSUM */
-#define SMAP_RUN_XOR          0x4u /* INDEX_WRITE/EDM: count and xr only (the cheapest fused reduction, E21) */
+#define SMAP_RUN_CHECKSUM     0x1u /* INDEX_WRITE(_ATM)/EDM: accumulate s0, s1 (E21) */
+#define SMAP_RUN_CHECKSUM_MIX 0x2u /* INDEX_WRITE(_ATM)/EDM: also accumulate mix (E21); implies CHECKSUM */
+#define SMAP_RUN_XOR          0x4u /* INDEX_WRITE(_ATM)/EDM: count and xr only (the cheapest fused reduction, E21) */
 
 typedef struct smap_plan_s *smap_plan_t;
 
@@ -182,7 +186,9 @@ smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes);
  *   flags:  SMAP_RUN_* bits.
  * The plan's result block is zeroed on the stream first; results are read with
  * smap_stats_fetch.  SMAP_E_INVALID: payload/m mismatch, missing points/out,
- * out_bytes too small, THREAD_DUMP with TILE granularity. */
+ * out_bytes too small, THREAD_DUMP with TILE granularity.
+ * SMAP_E_UNSUPPORTED: ATM / INDEX_WRITE_ATM with TILE rho > 32; ATM / TC /
+ * INDEX_WRITE_ATM on an inclusive plan. */
 smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float param,
                      void *out, size_t out_bytes, uint32_t flags, void *stream);
 

@@ -28,7 +28,7 @@ DIAG = {"strict": 0, "inclusive": 1}
 GRAN = {"thread": 0, "tile": 1}
 ORDER = {"rows": 0, "squares": 1}
 LAYOUT = {"rows": 0, "tiles": 1}
-PAYLOAD = {"index_write": 0, "edm": 1, "atm": 2, "tc": 3, "map_dump": 4, "hitcount": 5,
+PAYLOAD = {"index_write": 0, "edm": 1, "atm": 2, "tc": 3, "map_dump": 4, "hitcount": 5, "index_write_atm": 8,
            "thread_dump": 6, "empty": 7}
 DEVICE_NONE = -2          # smap_plan(device=DEVICE_NONE): host-only plan (validation + closed forms)
 RUN_CHECKSUM = 0x1
@@ -243,7 +243,7 @@ def out_dtype(plan: Plan, payload: str):
     import torch
     if payload == "edm":
         return torch.float32
-    if payload == "index_write":
+    if payload in ("index_write", "index_write_atm"):
         return torch.int64 if smap_volume(plan.m, plan.n, "inclusive" if plan.desc.diag else "strict") > (1 << 32) \
             else torch.int32
     if payload == "hitcount":

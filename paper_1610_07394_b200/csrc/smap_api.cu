@@ -224,6 +224,7 @@ static int internal_pl(smap_plan_t p, smap_payload pl)
     case SMAP_PAYLOAD_HITCOUNT: return PL_HIT;
     case SMAP_PAYLOAD_THREAD_DUMP: return PL_TDUMP;
     case SMAP_PAYLOAD_EMPTY: return PL_EMPTY;
+    case SMAP_PAYLOAD_INDEX_WRITE_ATM: return p->elem64 ? PL_IWA64 : PL_IWA32;
     }
     return -1;
 }
@@ -233,7 +234,8 @@ smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes)
     if (!p || !bytes) return fail(SMAP_E_INVALID, "smap_out_bytes: NULL argument");
     const uint64_t Vout = p->d.layout == SMAP_LAYOUT_TILES ? p->useful : p->V;   // tile layout: shard-local
     switch (pl) {
-    case SMAP_PAYLOAD_INDEX_WRITE: *bytes = (size_t)Vout * (p->elem64 ? 8 : 4); break;
+    case SMAP_PAYLOAD_INDEX_WRITE:
+    case SMAP_PAYLOAD_INDEX_WRITE_ATM: *bytes = (size_t)Vout * (p->elem64 ? 8 : 4); break;
     case SMAP_PAYLOAD_EDM: *bytes = (size_t)Vout * 4; break;
     case SMAP_PAYLOAD_HITCOUNT: *bytes = (size_t)Vout * 4; break;
     case SMAP_PAYLOAD_MAP_DUMP: *bytes = (size_t)p->P.nblocks * 16; break;
@@ -258,23 +260,24 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     const bool incl = d.diag == SMAP_DIAG_INCLUSIVE;
     if (flags & ~(SMAP_RUN_CHECKSUM | SMAP_RUN_CHECKSUM_MIX | SMAP_RUN_XOR)) return fail(SMAP_E_INVALID, "unknown flags 0x%x", flags);
     if (ipl == PL_EDM && (d.m != 2 || incl)) return fail(SMAP_E_INVALID, "EDM is defined on the m=2 strict domain");
-    if ((ipl == PL_ATM || ipl == PL_TC) && d.m != 3) return fail(SMAP_E_INVALID, "ATM/TC are m=3 payloads");
-    if ((ipl == PL_EDM || ipl == PL_ATM || ipl == PL_TC) && !points) return fail(SMAP_E_INVALID, "payload needs points");
-    if (ipl == PL_ATM && tile && d.m == 3 && d.rho > 32)
+    const bool atm = pl_atm(ipl);
+    if ((atm || ipl == PL_TC) && d.m != 3) return fail(SMAP_E_INVALID, "ATM/TC are m=3 payloads");
+    if ((ipl == PL_EDM || atm || ipl == PL_TC) && !points) return fail(SMAP_E_INVALID, "payload needs points");
+    if (atm && tile && d.m == 3 && d.rho > 32)
         return fail(SMAP_E_UNSUPPORTED, "ATM tiles are rho <= 32 (three rho x rho r^2 tables in shared memory)");
-    if ((ipl == PL_ATM || ipl == PL_TC) && d.diag == SMAP_DIAG_INCLUSIVE)
+    if ((atm || ipl == PL_TC) && d.diag == SMAP_DIAG_INCLUSIVE)
         return fail(SMAP_E_UNSUPPORTED, "ATM / TC are defined on distinct triples (strict diagonal)");
     if (ipl == PL_TDUMP && tile) return fail(SMAP_E_INVALID, "THREAD_DUMP needs THREAD granularity");
     size_t need = 0;
     smap_out_bytes(p, pl, &need);
     if (need > 0 && (!out || out_bytes < need))
         return fail(SMAP_E_INVALID, "out buffer too small: need %zu bytes, got %zu", need, out ? out_bytes : (size_t)0);
-    const bool csum_pl = ipl == PL_IW32 || ipl == PL_IW64 || ipl == PL_EDM;
+    const bool csum_pl = pl_iw(ipl) || ipl == PL_EDM;
     const int cs = !csum_pl ? 0 : (flags & SMAP_RUN_CHECKSUM_MIX) ? 2 : (flags & SMAP_RUN_CHECKSUM) ? 1
                                  : (flags & SMAP_RUN_XOR) ? 3 : 0;
     uint64_t rm = 1;
     for (int k = 0; k < d.m; k++) rm *= (uint64_t)d.rho;
-    const bool reduces = cs > 0 || ipl == PL_ATM || ipl == PL_TC;
+    const bool reduces = cs > 0 || atm || ipl == PL_TC;
     if (!tile && reduces && (rm % 32) != 0)
         return fail(SMAP_E_INVALID, "reductions need rho^m to be a multiple of 32 (rho^m = %llu)", (unsigned long long)rm);
 
@@ -286,7 +289,7 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     const int64_t npad = (int64_t)p->P.N * d.rho;          // bitmap over the padded index range
     if (tc_bits && (npad % 32) != 0) return fail(SMAP_E_UNSUPPORTED, "bit-sliced TC needs 2^ceil(log2 n) >= 32");
     if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)npad * (size_t)(npad / 32) * sizeof(uint32_t)));
-    if (ipl == PL_ATM) {
+    if (atm) {
         const uint64_t np = tile ? p->ctas : p->P.nblocks;
         if (np > p->npartials) {
             cudaFree(p->d_partials); cudaFree(p->d_scratch);
@@ -317,7 +320,7 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     if (e == cudaErrorInvalidValue) return fail(SMAP_E_UNSUPPORTED, "no kernel for this plan/payload combination");
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     launches++;
-    if (ipl == PL_ATM) {
+    if (atm) {
         const uint64_t np = tile ? p->ctas : p->P.nblocks;
         e = launch_finalize(p->d_partials, np, p->d_scratch, p->d_res, s, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "finalize launch");

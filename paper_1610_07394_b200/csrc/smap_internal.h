@@ -17,7 +17,12 @@ struct Result {
 };
 
 // Internal payload codes (the public smap_payload plus the index element width).
-enum Pl { PL_IW32 = 0, PL_IW64, PL_EDM, PL_ATM, PL_TC, PL_MAPD, PL_HIT, PL_TDUMP, PL_EMPTY };
+enum Pl { PL_IW32 = 0, PL_IW64, PL_EDM, PL_ATM, PL_TC, PL_MAPD, PL_HIT, PL_TDUMP, PL_EMPTY,
+          PL_IWA32, PL_IWA64 };   // IWA: index write + ATM sum in one pass (C3)
+// payload traits: writes packed indices / accumulates ATM terms / index element width
+constexpr bool pl_iw(int pl) { return pl == PL_IW32 || pl == PL_IW64 || pl == PL_IWA32 || pl == PL_IWA64; }
+constexpr bool pl_atm(int pl) { return pl == PL_ATM || pl == PL_IWA32 || pl == PL_IWA64; }
+constexpr int pl_iw_width(int pl) { return (pl == PL_IW64 || pl == PL_IWA64) ? PL_IW64 : PL_IW32; }
 
 struct Params {
     int n;          // elements per side (any n; the grid covers N * rho >= n)

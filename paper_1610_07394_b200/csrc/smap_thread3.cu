@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
     }
     // blocks with no element at all exit as a whole (lambda: idle spare/filler; BB: outside)
     if (PL != PL_TDUMP && ((LAM && B.cls == 3) || (!LAM && B.cls == 4))) {
-        if (PL == PL_ATM) {               // ATM writes one partial per block
+        if (pl_atm(PL)) {                 // ATM writes one partial per block
             if (a == 0 && bb == 0 && c == 0) P.partials[bid] = 0.0;
         }
         return;
@@ -61,17 +61,20 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
         return;
     }
 
-    if (PL == PL_IW32 || PL == PL_IW64 || PL == PL_HIT) {
+    if (pl_iw(PL) || PL == PL_HIT) {
+        constexpr int WPL = pl_iw_width(PL);
         Acc<CS> acc;
         if (valid) {
-            if (PL == PL_IW32) { reinterpret_cast<uint32_t *>(P.out)[p] = (uint32_t)p; acc.add(p, p); }
-            if (PL == PL_IW64) { reinterpret_cast<uint64_t *>(P.out)[p] = p; acc.add(p, p); }
             if (PL == PL_HIT) atomicAdd(reinterpret_cast<unsigned int *>(P.out) + p, 1u);
+            else if (WPL == PL_IW32) { reinterpret_cast<uint32_t *>(P.out)[p] = (uint32_t)p; acc.add(p, p); }
+            else { reinterpret_cast<uint64_t *>(P.out)[p] = p; acc.add(p, p); }
         }
-        if (CS > 0) block_add_slots<cs_mask<CS>()>(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid, acc.xr);
-        return;
+        // IWA: the ATM half below counts the block's elements
+        constexpr int MASK = pl_atm(PL) ? (cs_mask<CS>() & ~kMaskCount) : cs_mask<CS>();
+        if (MASK != 0) block_add_slots<MASK>(acc.count, acc.s0, acc.s1, acc.mix, 0, P.res, bid, acc.xr);
+        if (!pl_atm(PL)) return;
     }
-    if (PL == PL_ATM || PL == PL_TC) {
+    if (pl_atm(PL) || PL == PL_TC) {
         // stage the block's three point blocks (I, J, K) in shared memory once
         // (measured faster than per-thread loads: 9 scattered LDG per thread)
         __shared__ float4 sp[3 * 8];
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
         if (LAM) cnt = B.cls == 2 ? body : (B.I < B.J ? r3 : face);
         else cnt = B.cls == 0 ? r3 : (B.cls == 2 ? body : face / 2);
         if ((B.K + 1) * rho > (uint32_t)P.n) cnt = __syncthreads_count(valid);   // block cut by n (block-uniform)
-        if (PL == PL_ATM) {
+        if (pl_atm(PL)) {
             const double t = valid ? (double)atm_term(rij, rjk, rik, P.param) : 0.0;
             const double s = block_sum_f64(t);
             if (tid == 0) {
@@ -134,6 +137,8 @@ static cudaError_t pick3(const Params &P, int pl, int cs, cudaStream_t s)
     }
     CS3(PL_IW32)
     CS3(PL_IW64)
+    CS3(PL_IWA32)
+    CS3(PL_IWA64)
 #undef CS3
     if (pl == PL_ATM) return go3<MAP, PL_ATM, 0>(P, s);
     if (pl == PL_TC) return go3<MAP, PL_TC, 0>(P, s);

@@ -105,6 +105,11 @@ def main():
             ("tile_rho32_tiles_xor", dict(rho=32, granularity="tile", layout="tiles", flags=sm.RUN_XOR))],
             out=out, reps=a.reps)
         table["configs"]["C3_atm"] = compare(3, n, "atm", var, pts=p, param=1e-2, reps=a.reps)
+        # the config as stated: index write plus ATM sum, fused in one pass
+        table["configs"]["C3_index_write_atm"] = compare(3, n, "index_write_atm", var + [
+            ("tile_rho16_tiles_xor", dict(rho=16, granularity="tile", layout="tiles", flags=sm.RUN_XOR)),
+            ("tile_rho32_tiles_xor", dict(rho=32, granularity="tile", layout="tiles", flags=sm.RUN_XOR))],
+            pts=p, param=1e-2, out=out, reps=a.reps)
         del out
     if "C4" in only:
         n = 1 << 17

@@ -39,6 +39,7 @@ BENCH_EDM_VARIANTS = [BENCH_EDM, dict(rho=16, granularity="thread", map="lambda"
                       dict(rho=128, granularity="tile", map="lambda", layout="tiles")]
 BENCH_M3 = dict(rho=32, granularity="tile", map="lambda")
 BENCH_M3_VARIANTS = [BENCH_M3, dict(rho=8, granularity="thread", map="lambda")]
+BENCH_C3 = dict(rho=32, granularity="tile", map="lambda", layout="tiles")   # fused index write + ATM (E26)
 BENCH_C4 = dict(rho=128, granularity="tile", map="lambda", layout="tiles")
 BENCH_C5 = dict(rho=64, granularity="tile", map="lambda")         # TC: 64-bit predicate rows
 
