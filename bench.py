@@ -194,6 +194,94 @@ def combine_records(gathered):
     return out
 
 
+# ------------------------------------------------------------------ the other BASELINE configs (N = 1)
+def config_table(sm, torch, stream, peak_gbs, reps=10):
+    """Device time of every BASELINE.json config's product launch next to the
+    bounding box at the same launch and at the paper's one-element-per-thread
+    launch: CUDA events on the launching stream, 2 warm-ups,
+    median of `reps`.  Same payload code for both maps (BB is never inflated).
+    Each entry names its bound; HBM-bound entries carry achieved GB/s =
+    algorithmic bytes (V x element size) / time."""
+    import math
+
+    def med(plan, payload, pts=None, param=0.0, out=None, flags=0, k=reps):
+        for _ in range(2):
+            sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags, stream=stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        for a, b in ev:
+            a.record(stream)
+            sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags, stream=stream)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ts = sorted(a.elapsed_time(b) for a, b in ev)
+        return ts[len(ts) // 2]
+
+    def pair(m, n, payload, cfg, pts=None, param=0.0, out=None, flags=0, k=reps):
+        c = dict(cfg)
+        lam = sm.smap_plan(m, n, map="lambda", **c)
+        c.pop("order", None)
+        bb = sm.smap_plan(m, n, map="bb", **c)
+        ql, qb = sm.smap_plan_query(lam), sm.smap_plan_query(bb)
+        tl = med(lam, payload, pts, param, out, flags, k)
+        tb = med(bb, payload, pts, param, out, flags, k)
+        st = sm.smap_stats_fetch(lam)
+        V = ql["useful_elems"]
+        return {"launch": cfg, "lambda_ms": round(tl, 4), "bb_ms": round(tb, 4), "speedup_lambda_vs_bb": round(tb / tl, 3),
+                "launch_ratio": round(qb["launched_threads"] / ql["launched_threads"], 4),
+                "elements_per_s": V / (tl * 1e-3), "flags": flags,
+                "count_ok": st["count"] == V if (flags or payload in ("tc", "atm", "index_write_atm")) else None}, st
+
+    T = dict(granularity="tile", layout="tiles")
+    res = {}
+    # C1: m=2 n=1024 index write, 16x16 blocks (the paper's launch); launch-latency bound
+    n = workloads.CONFIGS["C1"]["n"]
+    out = torch.empty(sm.smap_volume(2, n), dtype=torch.int32, device=stream.device)
+    e, _ = pair(2, n, "index_write", dict(rho=16, granularity="thread"), out=out, flags=sm.RUN_XOR)
+    e["bound"] = "launch latency (2.1 MB of output)"
+    res["C1"] = {"product": e}
+    # C3: m=3 n=1024 index write + ATM sum, fused in one pass (tile 32, E26 layout)
+    c3 = workloads.CONFIGS["C3"]
+    n = c3["n"]
+    V3 = math.comb(n, 3)
+    pts3 = torch.from_numpy(workloads.points(n, workloads.SEED_C3)).to(stream.device)
+    out = torch.empty(V3, dtype=torch.int32, device=stream.device)
+    e, st = pair(3, n, "index_write_atm", {k: v for k, v in workloads.BENCH_C3.items() if k != "map"},
+                 pts=pts3, param=c3["eps2"], out=out, flags=sm.RUN_XOR)
+    p1 = sm.smap_plan(3, n, **workloads.BENCH_C3)
+    t_iw = med(p1, "index_write", out=out, flags=sm.RUN_XOR)
+    t_atm = med(p1, "atm", pts=pts3, param=c3["eps2"])
+    gbs = V3 * 4 / (e["lambda_ms"] * 1e-3) / 1e9
+    e.update(bound="FMA pipe (ATM terms) with the 714 MB index write riding along", atm_sum=st["sum"],
+             separate_passes_ms={"index_write": round(t_iw, 4), "atm": round(t_atm, 4)},
+             fused_vs_separate=round((t_iw + t_atm) / e["lambda_ms"], 3),
+             index_write_gbs=round(gbs, 1), index_write_frac_of_peak=round(gbs / peak_gbs, 4))
+    th, _ = pair(3, n, "index_write_atm", dict(rho=8, granularity="thread"), pts=pts3, param=c3["eps2"], out=out,
+                 flags=sm.RUN_XOR, k=max(3, reps // 2))
+    res["C3"] = {"product": e, "paper_launch": th}
+    del out
+    # C4: m=2 n=2^17 u64 index write (68.7 GB), tile 128, E23 layout; HBM-write bound
+    n = workloads.CONFIGS["C4"]["n"]
+    V4 = sm.smap_volume(2, n)
+    out = torch.empty(V4, dtype=torch.int64, device=stream.device)
+    e, _ = pair(2, n, "index_write", {k: v for k, v in workloads.BENCH_C4.items() if k != "map"}, out=out,
+                flags=sm.RUN_XOR, k=max(3, reps // 3))
+    gbs = V4 * 8 / (e["lambda_ms"] * 1e-3) / 1e9
+    e.update(bound="hbm (write)", achieved_gbs=round(gbs, 1), frac_of_peak=round(gbs / peak_gbs, 4))
+    th, _ = pair(2, n, "index_write", dict(rho=16, granularity="thread"), out=out, k=3)   # no fused reduction
+    res["C4"] = {"product": e, "paper_launch": th}
+    del out
+    torch.cuda.empty_cache()
+    # C5: m=3 n=2048 triple correlation count, tile 64 (64-bit predicate rows); issue bound
+    c5 = workloads.CONFIGS["C5"]
+    n = c5["n"]
+    pts5 = torch.from_numpy(workloads.points(n, workloads.SEED_C5)).to(stream.device)
+    e, st = pair(3, n, "tc", {k: v for k, v in workloads.BENCH_C5.items() if k != "map"}, pts=pts5, param=c5["R"])
+    e.update(bound="issue (AND + POPC per 64 triples, bitmap pre-pass included)", tc=st["tc"])
+    th, _ = pair(3, n, "tc", dict(rho=8, granularity="thread"), pts=pts5, param=c5["R"], k=max(3, reps // 2))
+    res["C5"] = {"product": e, "paper_launch": th}
+    return res
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -382,6 +470,12 @@ def main():
                 "write_fill_gbs_measured": round(fill, 1) if fill else None,
                 "frac_of_write_fill": round(achieved / fill, 4) if fill else None}
 
+    configs = None
+    if G == 1 and not args.no_compare:
+        del out
+        torch.cuda.empty_cache()
+        configs = config_table(sm, torch, stream, peak)
+
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         try:
@@ -403,6 +497,7 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clk,
             "lambda_vs_bb": compare,
+            "configs": configs,
             "checksum_ok": bool(ok),
             "result": {k: res[k] for k in ("count", "xr")},
         }
