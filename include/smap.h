@@ -51,12 +51,19 @@ typedef enum {
 typedef enum {
     SMAP_MAP_BB = 0,         /* bounding box: identity + filter */
     SMAP_MAP_LAMBDA = 1,     /* lambda2 / lambda3 reading R3 */
-    SMAP_MAP_ENUM = 2        /* comparison baseline: the linear-enumeration map
+    SMAP_MAP_ENUM = 2,       /* comparison baseline: the linear-enumeration map
                                 g: Z^1 -> Z^m of P:166-174, block-space as in P:252-262, inverted by
                                 the analytic root (fp32 sqrt for m=2, cbrt + sqrt for m=3, then an
                                 exact integer correction).  A 1-D grid of the N(N+1)/2 blocks J<=I
                                 (m=2) or the C(N+2,3) blocks I<=J<=K (m=3); diagonal blocks filter
                                 like BB.  THREAD granularity, unsharded. */
+    SMAP_MAP_BELOW = 3       /* "approach n from below" (reading E28): the M = ceil(n'/rho)
+                                tiles per side are cut into the binary digits of M (segments
+                                S_s = [O_s, O_s + N_s), N_0 > N_1 > ...); every piece is a power-of-two
+                                simplex mapped by lambda (lambda2 inclusive tile grid, lambda3 for
+                                N_s >= 8) or a box / small simplex at the identity, so every launched
+                                tile holds elements (besides lambda3's own idle tiles).  Any n; TILE
+                                granularity, canonical layout, unsharded. */
 } smap_map;
 
 typedef enum {
@@ -257,6 +264,14 @@ int smap_abi_version(void);
  *   lambda3: bid = (wz*(N/2) + wy)*W + (wx - wx0), wz in [0, 3N/4)
  *   BB2:     bid = I*N + J;   BB3: bid = (K*N + J)*N + I
  *   ENUM2:   bid = I(I+1)/2 + J, J <= I;   ENUM3: bid = C(K+2,3) + C(J+1,2) + I, I <= J <= K
+ *   BELOW:   pieces in order (m=2: for s = 0, 1, ...: triangle of S_s, then the rectangles
+ *            S_a x S_s, a < s; m=3: segment triples a <= b <= c, c outer, then b, then a);
+ *            inside a piece the lower-ranked coordinates vary fastest (rectangle: J, then I;
+ *            a < b = c: the line I, then the lambda2 inclusive grid id in row order;
+ *            a = b < c: the grid id, then K; box: I, J, K).  Records: m=2
+ *            {J, I, 0, cls} with cls 0 off-diagonal, 2 diagonal tile; m=3 {I, J, K, cls}
+ *            with cls 0/1/2/3 as lambda3 inside lambda3 pieces, else 0 interior,
+ *            5 I=J<K, 6 I<J=K, 2 I=J=K.
  * Threads (THREAD_DUMP order): t = ty*rho + tx (m=2); t = (c*rho + b)*rho + a (m=3). */
 
 #ifdef __cplusplus

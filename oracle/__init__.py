@@ -82,6 +82,9 @@ _SIGS = {
     "or_cs_tiles2": (i32, [i32, u64, u64, i32, i32, u64, u64, P, i32, P]),
     "or_tile_layout3": (i32, [u64, u64, i32, u64, u64, P, u64]),
     "or_cs_tiles3": (i32, [u64, u64, i32, u64, u64, i32, P]),
+    "or_below_segments": (i32, [u64, P, P]),
+    "or_below_tiles": (u64, [i32, u64, P]),
+    "or_below_element_hits": (i32, [i32, i32, u64, u64, P, u64, P]),
 }
 
 
@@ -354,3 +357,28 @@ def cs_edm(points, lo=0, hi=None, nthreads=0):
     cs = np.zeros(5, np.uint64)
     lib().or_cs_edm(n, _ptr(p), lo, n if hi is None else hi, nthreads, _ptr(cs))
     return dict(zip(CS_KEYS, (int(v) for v in cs)))
+
+
+# ------------------------------------------------------------------ approach n from below (reading E28)
+def below_segments(M):
+    """(sizes, offsets) of the binary-digit segments of M tiles."""
+    Ns, Os = np.zeros(64, np.uint64), np.zeros(64, np.uint64)
+    p = lib().or_below_segments(M, _ptr(Ns), _ptr(Os))
+    return [int(x) for x in Ns[:p]], [int(x) for x in Os[:p]]
+
+
+def below_tiles(m, M) -> np.ndarray:
+    """Tile records {x0, x1, x2, cls} of the below decomposition in launch order."""
+    cnt = lib().or_below_tiles(m, M, None)
+    out = np.zeros((cnt, 4), np.int32)
+    lib().or_below_tiles(m, M, _ptr(out))
+    return out
+
+
+def below_element_hits(m, inclusive, n, T):
+    """(hits per packed rank, {tiles, useful, outside}) of the below decomposition."""
+    V = domain_volume(m, inclusive, n)
+    hits = np.zeros(V, np.uint32)
+    res = np.zeros(3, np.int64)
+    assert lib().or_below_element_hits(m, int(inclusive), n, T, _ptr(hits), V, _ptr(res)) == 0
+    return hits, dict(zip(("tiles", "useful", "outside"), (int(x) for x in res)))

@@ -1123,3 +1123,193 @@ int or_map_dump(int m, int inclusive, int map, uint64_t N, uint64_t rank, uint64
     }
     return 0;
 }
+
+/* ======================================================================
+ * "Approach n from below" (reading E28 in DESIGN.md), at tile
+ * level.  P:399-404 reads: apply orthotopes Pi_{n_1}, Pi_{n_2}, ... with
+ * n_1 = floor(log2 n) and n_i = log2(n - sum_{k<i} n_k), "plus a set of more
+ * simpler mappings for the sub-orthotopes that remain un-mapped at each
+ * level".  The printed n_i are logarithms where sizes are meant (reading
+ * E7): the sizes are 2^floor(log2(n - sum_{k<i} n_k)), i.e. the binary
+ * digits of n in descending order.  Applied to the M = ceil(n'/T) tiles per
+ * side (n' = n, or n + 2 for the m = 3 inclusive set of reading E24):
+ *   segments   S_s = [O_s, O_s + N_s), N_0 > N_1 > ... the binary digits of M,
+ *              O_s = N_0 + ... + N_{s-1};
+ *   m = 2      for s = 0, 1, ...: the triangle of S_s by lambda2
+ *              over the inclusive tile grid (N_s/2) x (N_s + 1) (grid rows 0
+ *              and N_s hold one diagonal tile each, reading E6; N_s = 1: the
+ *              single diagonal tile), then the "simpler mappings" of the
+ *              rectangles S_a x S_s, a < s, at the identity (J fastest);
+ *   m = 3      for every segment triple a <= b <= c (c outer, then b, then a):
+ *              a = b = c  the tetrahedron of S_a by lambda3 (reading R3) over
+ *                         its (N/2, N/2, 3N/4) tile grid for N_a >= 8; for
+ *                         N_a < 8 the C(N_a + 2, 3) tiles I <= J <= K in colex
+ *                         order (a "simpler mapping");
+ *              a < b = c  S_a x (triangle J <= K of S_b by the lambda2 grid above);
+ *              a = b < c  (triangle I <= J of S_a by the lambda2 grid) x S_c;
+ *              a < b < c  the box S_a x S_b x S_c at the identity.
+ * Inside a piece the lower-ranked coordinates vary fastest (the order of the
+ * packed layout): rectangle J then I; a < b = c the line I, then the lambda2
+ * grid id (row order); a = b < c the lambda2 grid id, then K; box I, J, K.  Records have the
+ * MAP_DUMP format {x0, x1, x2, cls}: m = 2 {J, I, 0, cls} with cls 0
+ * off-diagonal, 2 diagonal tile; m = 3 {I, J, K, cls} with cls 0/1 the lambda3
+ * branch (I = J: a face tile carrying {I=J<K} and {I<J=K}), 2 body tile,
+ * 3 idle lambda3 tile (zeros), and for the other pieces cls 0 interior
+ * (I < J < K), 5 face I = J < K, 6 face I < J = K, 2 body (I = J = K).
+ * ====================================================================== */
+int or_below_segments(uint64_t M, uint64_t *Ns, uint64_t *Os)
+{
+    int p = 0;
+    uint64_t rest = M, off = 0;
+    while (rest > 0) {
+        uint64_t b = or_pow2(or_floor_log2(rest));   /* 2^floor(log2(M - sum so far)) */
+        Ns[p] = b; Os[p] = off;
+        off += b; rest -= b; p++;
+    }
+    return p;
+}
+
+/* the (J, K) tile of grid id g of the lambda2 inclusive tile grid of side N
+ * (J <= K; returns 1 for a diagonal tile) */
+static int or_below_tri(uint64_t N, uint64_t g, uint64_t *J, uint64_t *K)
+{
+    if (N == 1) { *J = *K = 0; return 1; }
+    uint64_t W = N / 2, wx = g % W, wy = g / W;
+    if (wy == 0) { *J = *K = wx; return 1; }
+    if (wy == N) { *J = *K = wx + N / 2; return 1; }
+    or_lambda2(wx, wy, J, K);
+    return 0;
+}
+
+static uint64_t or_below_tri_count(uint64_t N) { return N == 1 ? 1 : (N / 2) * (N + 1); }
+
+static void or_rec4(int32_t *r, uint64_t a, uint64_t b, uint64_t c, int cls)
+{
+    r[0] = (int32_t)a; r[1] = (int32_t)b; r[2] = (int32_t)c; r[3] = cls;
+}
+
+/* Tile records of the below decomposition in launch order; returns the
+ * number of tiles (out may be NULL to count only). */
+uint64_t or_below_tiles(int m, uint64_t M, int32_t *out)
+{
+    uint64_t Ns[64], Os[64], cnt = 0;
+    int p = or_below_segments(M, Ns, Os);
+    if (m == 2) {
+        for (int s = 0; s < p; s++) {
+            for (uint64_t g = 0; g < or_below_tri_count(Ns[s]); g++, cnt++) {
+                uint64_t J, I;
+                int d = or_below_tri(Ns[s], g, &J, &I);
+                if (out) or_rec4(out + 4 * cnt, Os[s] + J, Os[s] + I, 0, d ? 2 : 0);
+            }
+            for (int a = 0; a < s; a++)           /* rectangle S_a x S_s, J fastest */
+                for (uint64_t g = 0; g < Ns[a] * Ns[s]; g++, cnt++)
+                    if (out) or_rec4(out + 4 * cnt, Os[a] + g % Ns[a], Os[s] + g / Ns[a], 0, 0);
+        }
+        return cnt;
+    }
+    for (int c = 0; c < p; c++)
+        for (int b = 0; b <= c; b++)
+            for (int a = 0; a <= b; a++) {
+                if (a == b && b == c) {
+                    uint64_t N = Ns[a], O = Os[a];
+                    if (N >= 8) {
+                        uint64_t nb = (N / 2) * (N / 2) * (3 * N / 4);
+                        for (uint64_t g = 0; g < nb; g++, cnt++) {
+                            if (!out) continue;
+                            uint64_t wx = g % (N / 2), wy = (g / (N / 2)) % (N / 2), wz = g / (N / 2) / (N / 2);
+                            int64_t o[6];
+                            int k = or_lambda3(N, wx, wy, wz, o);
+                            if (k == OR_L3_INSIDE || k == OR_L3_REFLECTED) or_rec4(out + 4 * cnt, O + o[3], O + o[4], O + o[5], k);
+                            else if (k == OR_L3_SPARE && o[0] >= 0) or_rec4(out + 4 * cnt, O + o[0], O + o[0], O + o[0], 2);
+                            else or_rec4(out + 4 * cnt, 0, 0, 0, 3);
+                        }
+                    } else {
+                        for (uint64_t K = 0; K < N; K++)
+                            for (uint64_t J = 0; J <= K; J++)
+                                for (uint64_t I = 0; I <= J; I++, cnt++) {
+                                    int cls = (I < J && J < K) ? 0 : (I == J && J < K) ? 5 : (I < J) ? 6 : 2;
+                                    if (out) or_rec4(out + 4 * cnt, O + I, O + J, O + K, cls);
+                                }
+                    }
+                } else if (b == c) {          /* a < b = c */
+                    for (uint64_t g = 0; g < Ns[a] * or_below_tri_count(Ns[b]); g++, cnt++) {
+                        uint64_t J, K;
+                        int d = or_below_tri(Ns[b], g / Ns[a], &J, &K);
+                        if (out) or_rec4(out + 4 * cnt, Os[a] + g % Ns[a], Os[b] + J, Os[b] + K, d ? 6 : 0);
+                    }
+                } else if (a == b) {          /* a = b < c: the triangle fastest, then K */
+                    uint64_t tc = or_below_tri_count(Ns[a]);
+                    for (uint64_t g = 0; g < Ns[c] * tc; g++, cnt++) {
+                        uint64_t I, J;
+                        int d = or_below_tri(Ns[a], g % tc, &I, &J);
+                        if (out) or_rec4(out + 4 * cnt, Os[a] + I, Os[a] + J, Os[c] + g / tc, d ? 5 : 0);
+                    }
+                } else {                      /* a < b < c */
+                    for (uint64_t g = 0; g < Ns[a] * Ns[b] * Ns[c]; g++, cnt++)
+                        if (out) or_rec4(out + 4 * cnt, Os[a] + g % Ns[a], Os[b] + (g / Ns[a]) % Ns[b],
+                                         Os[c] + g / Ns[a] / Ns[b], 0);
+                }
+            }
+    return cnt;
+}
+
+/* Element-level cover of the below decomposition: one hit per element the
+ * tile records carry (tile (I,J,K) holds the elements i = I*T + il etc.;
+ * diagonal tiles clip to the domain, elements with the largest index >= n'
+ * are filtered).  res = {tiles, useful, outside}. */
+int or_below_element_hits(int m, int inclusive, uint64_t n, uint64_t T, uint32_t *hits, uint64_t V, int64_t *res)
+{
+    uint64_t nint = (m == 3 && inclusive) ? n + 2 : n;      /* E24 */
+    uint64_t M = (nint + T - 1) / T;
+    uint64_t nt = or_below_tiles(m, M, NULL);
+    int32_t *rec = malloc(nt * 4 * sizeof(int32_t));
+    if (!rec) return -1;
+    or_below_tiles(m, M, rec);
+    int64_t useful = 0, outside = 0;
+    for (uint64_t t = 0; t < nt; t++) {
+        int32_t *r = rec + 4 * t;
+        if (m == 2) {
+            uint64_t J = (uint64_t)r[0], I = (uint64_t)r[1];
+            for (uint64_t rr = 0; rr < T; rr++)
+                for (uint64_t cc = 0; cc < T; cc++) {
+                    uint64_t i = I * T + rr, j = J * T + cc;
+                    if (i >= n) continue;
+                    if (r[3] == 2 && (inclusive ? cc > rr : cc >= rr)) continue;
+                    int in = inclusive ? j <= i : j < i;
+                    if (!in) { outside++; continue; }
+                    uint64_t p = inclusive ? or_rank2_incl(i, j) : or_rank2_strict(i, j);
+                    if (p >= V) { outside++; continue; }
+                    hits[p]++; useful++;
+                }
+            continue;
+        }
+        if (r[3] == 3) continue;
+        uint64_t I = (uint64_t)r[0], J = (uint64_t)r[1], K = (uint64_t)r[2];
+        or_seg3 sg[2];
+        int ns = 1;
+        if (r[3] == 2) { sg[0].I = sg[0].J = sg[0].K = I; sg[0].kind = 3; }
+        else if (I < J && J < K) { sg[0].I = I; sg[0].J = J; sg[0].K = K; sg[0].kind = 0; }
+        else if (r[3] == 5) { sg[0].I = I; sg[0].J = I; sg[0].K = K; sg[0].kind = 1; }
+        else if (r[3] == 6) { sg[0].I = I; sg[0].J = K; sg[0].K = K; sg[0].kind = 2; }
+        else {                                   /* lambda3 face tile I = J < K: both folded sets (E14) */
+            sg[0].I = I; sg[0].J = I; sg[0].K = K; sg[0].kind = 1;
+            sg[1].I = I; sg[1].J = K; sg[1].K = K; sg[1].kind = 2;
+            ns = 2;
+        }
+        for (int q = 0; q < ns; q++) {
+            uint64_t pos = 0;
+            OR_SEG3_WALK(sg[q], T, pos, {
+                if (k_ >= nint) continue;
+                uint64_t pp = rank_;
+                int in = i_ < j_ && j_ < k_;
+                if (in && inclusive) pp = or_rank3_incl(i_, j_ - 1, k_ - 2);
+                if (!in || pp >= V) { outside++; continue; }
+                hits[pp]++; useful++;
+            })
+            (void)pos;
+        }
+    }
+    free(rec);
+    res[0] = (int64_t)nt; res[1] = useful; res[2] = outside;
+    return 0;
+}

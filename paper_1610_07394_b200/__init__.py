@@ -23,7 +23,7 @@ _lib = C.CDLL(LIB_PATH)
 
 # ------------------------------------------------------------------ enums
 OK, E_INVALID, E_UNSUPPORTED, E_CUDA, E_NOMEM = range(5)
-MAP = {"bb": 0, "lambda": 1, "enum": 2}
+MAP = {"bb": 0, "lambda": 1, "enum": 2, "below": 3}
 DIAG = {"strict": 0, "inclusive": 1}
 GRAN = {"thread": 0, "tile": 1}
 ORDER = {"rows": 0, "squares": 1}

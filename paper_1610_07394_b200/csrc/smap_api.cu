@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "smap.h"
 #include "smap_device.cuh"
@@ -28,6 +29,8 @@ struct smap_plan_s {
     uint64_t npartials = 0;
     double *d_scratch = nullptr;
     uint32_t *d_adj = nullptr;      // TC pair-predicate bitmap (TILE)
+    Piece *d_pieces = nullptr;      // SMAP_MAP_BELOW decomposition
+    std::vector<Piece> pieces;
     float *d_stage = nullptr;
     smap_result *d_rec = nullptr;   // smap_run_host: device record
     smap_result *h_rec = nullptr;   // smap_run_host: pinned host record
@@ -65,6 +68,52 @@ static smap_status cuda_fail(cudaError_t e, const char *where)
 static bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 static int ilog2(int64_t x) { int l = 0; while ((int64_t)1 << (l + 1) <= x) l++; return l; }
 
+// "Approach n from below" (reading E28): the pieces of the M-tile
+// simplex in launch order (include/smap.h); returns the total tile count.
+static uint64_t below_pieces(int m, int64_t M, std::vector<Piece> &out)
+{
+    std::vector<uint32_t> Ns, Os;
+    for (int64_t rest = M, off = 0; rest > 0;) {        // binary digits of M, largest first
+        const int64_t b = (int64_t)1 << ilog2(rest);
+        Ns.push_back((uint32_t)b); Os.push_back((uint32_t)off);
+        off += b; rest -= b;
+    }
+    const int p = (int)Ns.size();
+    uint64_t start = 0;
+    auto add = [&](uint8_t kind, int a, int b, int c, uint64_t count) {
+        Piece pc;
+        pc.start = start; pc.kind = kind;
+        pc.Oa = Os[a]; pc.Ob = Os[b]; pc.Oc = Os[c];
+        pc.ea = (uint8_t)ilog2(Ns[a]); pc.eb = (uint8_t)ilog2(Ns[b]); pc.ec = (uint8_t)ilog2(Ns[c]);
+        out.push_back(pc);
+        start += count;
+    };
+    auto tri = [](uint64_t N) { return N == 1 ? (uint64_t)1 : (N / 2) * (N + 1); };   // lambda2 inclusive tile grid
+    if (m == 2) {
+        for (int s = 0; s < p; s++) {
+            add(PK_TRI2, s, s, s, tri(Ns[s]));
+            for (int a = 0; a < s; a++) add(PK_RECT2, a, s, s, (uint64_t)Ns[a] * Ns[s]);
+        }
+        return start;
+    }
+    for (int c = 0; c < p; c++)
+        for (int b = 0; b <= c; b++)
+            for (int a = 0; a <= b; a++) {
+                const uint64_t Na = Ns[a], Nb = Ns[b], Nc = Ns[c];
+                if (a == c) {
+                    if (Na >= 8) add(PK_TET3, a, a, a, (Na / 2) * (Na / 2) * (3 * Na / 4));
+                    else add(PK_TETS, a, a, a, Na * (Na + 1) * (Na + 2) / 6);
+                } else if (b == c) {
+                    add(PK_LT, a, b, c, Na * tri(Nb));
+                } else if (a == b) {
+                    add(PK_TL, a, b, c, Nc * tri(Na));
+                } else {
+                    add(PK_BOX, a, b, c, Na * Nb * Nc);
+                }
+            }
+    return start;
+}
+
 extern "C" {
 
 int smap_abi_version(void) { return SMAP_ABI_VERSION; }
@@ -94,10 +143,13 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     const bool tile = d->granularity == SMAP_GRAN_TILE;
     const int G = d->shard_count;
     if (m != 2 && m != 3) return fail(SMAP_E_INVALID, "m must be 2 or 3 (got %d)", m);
-    if (d->map != SMAP_MAP_BB && d->map != SMAP_MAP_LAMBDA && d->map != SMAP_MAP_ENUM)
+    if (d->map != SMAP_MAP_BB && d->map != SMAP_MAP_LAMBDA && d->map != SMAP_MAP_ENUM && d->map != SMAP_MAP_BELOW)
         return fail(SMAP_E_INVALID, "bad map %d", d->map);
     const bool enm = d->map == SMAP_MAP_ENUM;
+    const bool below = d->map == SMAP_MAP_BELOW;
     if (enm && tile) return fail(SMAP_E_INVALID, "the enumeration baseline map is THREAD granularity only");
+    if (below && !tile) return fail(SMAP_E_INVALID, "the approach-from-below map is TILE granularity only");
+    if (below && d->layout != SMAP_LAYOUT_ROWS) return fail(SMAP_E_UNSUPPORTED, "the approach-from-below map writes the canonical layout");
     if (d->diag != SMAP_DIAG_STRICT && d->diag != SMAP_DIAG_INCLUSIVE) return fail(SMAP_E_INVALID, "bad diag %d", d->diag);
     if (d->granularity != SMAP_GRAN_THREAD && d->granularity != SMAP_GRAN_TILE)
         return fail(SMAP_E_INVALID, "bad granularity %d", d->granularity);
@@ -111,7 +163,8 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     int64_t npad = 1;
     while (npad < nint) npad <<= 1;
     const bool padded = npad != nint;
-    if (!is_pow2(rho) || rho > npad) return fail(SMAP_E_INVALID, "rho must be a power of two <= 2^ceil(log2 n) (got %d)", rho);
+    if (!is_pow2(rho) || (rho > npad && !below))
+        return fail(SMAP_E_INVALID, "rho must be a power of two <= 2^ceil(log2 n) (got %d)", rho);
     if (!tile) {
         if ((m == 2 && rho > 32) || (m == 3 && rho > 8))
             return fail(SMAP_E_INVALID, "THREAD granularity needs rho^m <= 1024 (rho=%d, m=%d)", rho, m);
@@ -125,7 +178,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (m == 2 && lam && N < 2) return fail(SMAP_E_INVALID, "lambda2 needs N = n/rho >= 2");
     if (m == 3 && lam && N < 8) return fail(SMAP_E_INVALID, "lambda3 needs N = n/rho >= 8 (body blocks, E14)");
     if (G < 1 || !is_pow2(G)) return fail(SMAP_E_INVALID, "shard_count must be a power of two >= 1");
-    if (!lam && G != 1) return fail(SMAP_E_INVALID, "BB and ENUM plans are unsharded");
+    if (!lam && G != 1) return fail(SMAP_E_INVALID, "BB, ENUM and BELOW plans are unsharded");
     if (lam && (N / 2) % G != 0) return fail(SMAP_E_INVALID, "shard_count %d does not divide N/2 = %lld", G, (long long)(N / 2));
     if (d->shard_rank < 0 || d->shard_rank >= G) return fail(SMAP_E_INVALID, "shard_rank out of range");
     if (d->order != SMAP_ORDER_ROWS && d->order != SMAP_ORDER_SQUARES) return fail(SMAP_E_INVALID, "bad order %d", d->order);
@@ -144,7 +197,13 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     memset(&P, 0, sizeof P);
     P.n = (int)nint; P.N = (int)N; P.log2N = ilog2(N); P.rho = rho; P.log2rho = ilog2(rho);
     P.layout = d->layout;
-    if (lam) {
+    if (below) {                              // M = ceil(n'/rho) tiles per side, any M
+        const int64_t M = (nint + rho - 1) / rho;
+        P.N = (int)M; P.log2N = 0;
+        P.W = (int)M; P.log2W = 0; P.wx0 = 0;
+        P.nblocks = below_pieces(m, M, p->pieces);
+        P.npieces = (int)p->pieces.size();
+    } else if (lam) {
         P.W = (int)(N / 2 / G); P.log2W = ilog2(P.W); P.wx0 = d->shard_rank * P.W;
         P.order = m == 2 ? d->order : 0;
         P.nblocks = m == 2 ? (uint64_t)P.W * (uint64_t)(incl ? N + 1 : N)
@@ -198,6 +257,13 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
         return cuda_fail(e, "smap_plan scratch");
     }
     P.res = p->d_res;
+    if (below) {
+        e = cudaMalloc(&p->d_pieces, p->pieces.size() * sizeof(Piece));
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p->d_pieces, p->pieces.data(), p->pieces.size() * sizeof(Piece), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { smap_destroy(p); return cuda_fail(e, "smap_plan pieces"); }
+        P.pieces = p->d_pieces;
+    }
     *out = p;
     return SMAP_OK;
 }
@@ -315,8 +381,8 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
         launches++;
     }
     if (!tile) e = d.m == 2 ? launch_thread2(P, d.map, incl, ipl, cs, s) : launch_thread3(P, d.map, ipl, cs, s);
-    else e = d.m == 2 ? launch_tile2(P, d.rho, lam, incl, ipl, cs, p->ctas, s)
-                      : launch_tile3(P, d.rho, lam, ipl, cs, p->ctas, s);
+    else e = d.m == 2 ? launch_tile2(P, d.rho, d.map, incl, ipl, cs, p->ctas, s)
+                      : launch_tile3(P, d.rho, d.map, ipl, cs, p->ctas, s);
     if (e == cudaErrorInvalidValue) return fail(SMAP_E_UNSUPPORTED, "no kernel for this plan/payload combination");
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     launches++;
@@ -503,6 +569,7 @@ void smap_destroy(smap_plan_t p)
     if (p->d_partials) cudaFree(p->d_partials);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_adj) cudaFree(p->d_adj);
+    if (p->d_pieces) cudaFree(p->d_pieces);
     if (p->d_stage) cudaFree(p->d_stage);
     if (p->d_rec) cudaFree(p->d_rec);
     if (p->h_rec) cudaFreeHost(p->h_rec);

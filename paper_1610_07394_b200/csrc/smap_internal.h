@@ -24,6 +24,24 @@ constexpr bool pl_iw(int pl) { return pl == PL_IW32 || pl == PL_IW64 || pl == PL
 constexpr bool pl_atm(int pl) { return pl == PL_ATM || pl == PL_IWA32 || pl == PL_IWA64; }
 constexpr int pl_iw_width(int pl) { return (pl == PL_IW64 || pl == PL_IWA64) ? PL_IW64 : PL_IW32; }
 
+// "Approach n from below" (reading E28): the M tiles per side are
+// cut into the binary-digit segments of M; every piece of the decomposition
+// is a power-of-two simplex mapped by lambda or a box at the identity.
+enum PieceKind {
+    PK_TRI2 = 0,   // m=2: triangle of segment a (lambda2 inclusive tile grid; N_a = 1: one diagonal tile)
+    PK_RECT2,      // m=2: rectangle J in segment a x I in segment b, a < b (identity)
+    PK_TET3,       // m=3: tetrahedron of segment a by lambda3 (R3), N_a >= 8
+    PK_TETS,       // m=3: tetrahedron of segment a, N_a < 8: tiles I <= J <= K in colex order
+    PK_LT,         // m=3: I in segment a  x  triangle J <= K of segment b (lambda2 grid)
+    PK_TL,         // m=3: triangle I <= J of segment a (lambda2 grid)  x  K in segment c
+    PK_BOX         // m=3: segments a < b < c at the identity
+};
+struct Piece {
+    uint64_t start;            // first tile id of the piece (launch order)
+    uint32_t Oa, Ob, Oc;       // segment offsets (tiles)
+    uint8_t kind, ea, eb, ec;  // PieceKind, log2 of the segment sizes
+};
+
 struct Params {
     int n;          // elements per side (any n; the grid covers N * rho >= n)
     int N;          // blocks (tiles) per side = n / rho
@@ -42,6 +60,8 @@ struct Params {
     Result *res;
     double *partials;              // ATM: one fp64 per CTA
     const uint32_t *adj;           // TC (TILE): pair-predicate bitmap, n rows of n/32 words
+    const Piece *pieces;           // SMAP_MAP_BELOW: the decomposition, sorted by start
+    int npieces;
 };
 
 // ---------------------------------------------------------------- m=3 tile-blocked layout (E26)
@@ -117,8 +137,8 @@ __host__ __device__ __forceinline__ uint64_t seg3_local(int kind, uint64_t il, u
 // for a combination that has no instantiated kernel.
 cudaError_t launch_thread2(const Params &P, int map, bool incl, int pl, int cs, cudaStream_t s);
 cudaError_t launch_thread3(const Params &P, int map, int pl, int cs, cudaStream_t s);
-cudaError_t launch_tile2(const Params &P, int T, bool lam, bool incl, int pl, int cs, unsigned ctas, cudaStream_t s);
-cudaError_t launch_tile3(const Params &P, int T, bool lam, int pl, int cs, unsigned ctas, cudaStream_t s);
+cudaError_t launch_tile2(const Params &P, int T, int map, bool incl, int pl, int cs, unsigned ctas, cudaStream_t s);
+cudaError_t launch_tile3(const Params &P, int T, int map, int pl, int cs, unsigned ctas, cudaStream_t s);
 // TC pre-pass: adj[j * (npad/32) + w] bit b <=> 32w + b < n, j < n and
 // r2(32w + b, j) < R*R (the same fp32 predicate as the per-triple compare);
 // npad = N * rho, a multiple of 32.

@@ -1,0 +1,70 @@
+"""Approach n from below (SMAP_MAP_BELOW) vs approach n from above
+(the padded lambda grid) vs the bounding box, at non-power-of-two
+n: device time (CUDA events, median of reps) and launched tiles.  Writes
+gpurun_out/below.json.
+
+    python scripts/below_bench.py [--reps 10]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+import paper_1610_07394_b200 as sm
+import workloads
+
+
+def med(plan, payload, pts=None, param=0.0, out=None, flags=0, reps=10):
+    for _ in range(2):
+        sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record()
+        sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags)
+        b.record()
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in ev)
+    return ts[len(ts) // 2]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=10)
+    a = ap.parse_args()
+    rows = []
+    cases = [(2, 40000, "edm", 128, workloads.SEED_C2, 0.0), (2, 70000, "edm", 128, workloads.SEED_C2, 0.0),
+             (2, 100000, "index_write", 128, None, 0.0),
+             (3, 1100, "index_write", 32, None, 0.0), (3, 1100, "atm", 32, workloads.SEED_C3, 1e-2),
+             (3, 1500, "atm", 32, workloads.SEED_C3, 1e-2), (3, 2100, "tc", 64, workloads.SEED_C5, 0.5),
+             (3, 3000, "tc", 64, workloads.SEED_C5, 0.5)]
+    for m, n, payload, T, seed, param in cases:
+        pts = torch.from_numpy(workloads.points(n, seed)).cuda() if seed else None
+        row = {"m": m, "n": n, "payload": payload, "tile": T, "elements": sm.smap_volume(m, n)}
+        out = None
+        for mp in ("below", "lambda", "bb"):
+            plan = sm.smap_plan(m, n, T, map=mp, granularity="tile")
+            if out is None:
+                out = sm.alloc_out(plan, payload)
+            flags = sm.RUN_XOR if payload in ("edm", "index_write") else 0
+            ms = med(plan, payload, pts, param, out, flags, a.reps)
+            st = sm.smap_stats_fetch(plan)
+            q = sm.smap_plan_query(plan)
+            row[mp] = {"ms": round(ms, 4), "tiles": q["grid_blocks"], "count": st["count"]}
+        row["above_over_below"] = round(row["lambda"]["ms"] / row["below"]["ms"], 3)
+        row["bb_over_below"] = round(row["bb"]["ms"] / row["below"]["ms"], 3)
+        print(json.dumps(row), flush=True)
+        rows.append(row)
+        del out
+        torch.cuda.empty_cache()
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/below.json", "w") as f:
+        json.dump({"device": torch.cuda.get_device_name(0), "rows": rows}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
