@@ -105,7 +105,7 @@ def test_c5_tc_full(sm, orc):
     n = c["n"]
     p = workloads.points(n, workloads.SEED_C5)
     ref = orc.tc_count(p, np.float32(c["R"]))
-    for cfg in workloads.BENCH_M3_VARIANTS + [dict(rho=64, granularity="tile", map="lambda")]:
+    for cfg in workloads.BENCH_M3_VARIANTS + [dict(rho=64, granularity="tile", map="lambda"), workloads.BENCH_C5]:
         plan = sm.smap_plan(3, n, **cfg)
         sm.smap_run(plan, "tc", points=torch.from_numpy(p).cuda(), param=c["R"])
         st = sm.smap_stats_fetch(plan)

@@ -41,7 +41,7 @@ BENCH_M3 = dict(rho=32, granularity="tile", map="lambda")
 BENCH_M3_VARIANTS = [BENCH_M3, dict(rho=8, granularity="thread", map="lambda")]
 BENCH_C3 = dict(rho=32, granularity="tile", map="lambda", layout="tiles")   # fused index write + ATM (E26)
 BENCH_C4 = dict(rho=128, granularity="tile", map="lambda", layout="tiles")
-BENCH_C5 = dict(rho=64, granularity="tile", map="lambda")         # TC: 64-bit predicate rows
+BENCH_C5 = dict(rho=64, granularity="tile", map="lambda", persistent=8)   # TC: 64-bit predicate rows, 8 CTAs/SM
 
 
 def points(n: int, seed: int) -> np.ndarray:
