@@ -180,9 +180,9 @@ def run_reference(args):
 
 
 def combine_records(gathered):
-    """Combine G smap_result records (G x 7 int64: count s0 s1 mix tc xr sum):
-    integer fields add mod 2^64, xr combines by xor (NCCL has no bitwise
-    reduction), the fp64 sum adds."""
+    """Reference (torch ops) for smap_result_combine: combine G smap_result
+    records (G x 7 int64: count s0 s1 mix tc xr sum): integer fields add mod
+    2^64, xr combines by xor (NCCL has no bitwise reduction), the fp64 sum adds."""
     import torch
     out = torch.empty_like(gathered[0])
     out[:5] = gathered[:, :5].sum(0)
@@ -326,9 +326,9 @@ def main():
     flags = sm.RUN_XOR
 
     def combine():
-        # a8: one all-gather of the 56-byte records, combined on the device
+        # a8: one all-gather of the 56-byte records, combined on the device by one kernel
         dist.all_gather_into_tensor(gathered, rec)
-        rec.copy_(combine_records(gathered.view(G, 7)))
+        sm.smap_result_combine(gathered, G, rec, stream=stream)
 
     def step():
         sm.smap_run(plan, "edm", points=pts, out=out, flags=flags, stream=stream)
@@ -366,7 +366,7 @@ def main():
     ms_local = t0.elapsed_time(t1) / args.steps
     kern_ms_local = sum(a.elapsed_time(b) for a, b in zip(ke0, ke1)) / args.steps
     res = sm.result_dict(rec)
-    launches_per_step = sm.smap_stats_fetch(plan)["launches"] + 1
+    launches_per_step = sm.smap_stats_fetch(plan)["launches"] + 1 + (1 if G > 1 else 0)   # + reduce (+ combine)
     tm = torch.tensor([ms_local, kern_ms_local], dtype=torch.float64, device=dev)
     if G > 1:
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)

@@ -225,6 +225,15 @@ typedef struct {
  * count/s0/s1/mix/tc add exactly mod 2^64, xr combines by xor, sum adds in fp64. */
 smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream);
 
+/* Combine `count` smap_result records at the DEVICE address `records`
+ * (contiguous, e.g. the output of an all-gather of every rank's record) into
+ * one record at the DEVICE address `dst`, asynchronously on `stream` (one
+ * one-warp kernel): count/s0/s1/mix/tc add mod 2^64, xr combines by xor, the
+ * fp64 sums add in record order 0..count-1 (deterministic).  Both pointers
+ * 8-byte aligned; dst may alias records[0].  SMAP_E_INVALID on NULL pointers,
+ * misalignment or count < 1. */
+smap_status smap_result_combine(const void *records, int count, void *dst, void *stream);
+
 /* Where element e lives (m=2: e = {i, j}, j < i (<= i inclusive); m=3: e = {i, j, k}):
  * *shard = the shard rank that writes it, *pos = its position in that shard's
  * `out` array (SMAP_LAYOUT_ROWS: the packed rank in the full-size array;

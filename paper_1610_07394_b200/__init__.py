@@ -68,6 +68,7 @@ _SIGS = {
     "smap_run_host": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_size_t, C.c_uint32, _P, C.POINTER(Stats)]),
     "smap_stats_fetch": (C.c_int, [_P, C.POINTER(Stats)]),
     "smap_result_reduce": (C.c_int, [_P, _P, _P]),
+    "smap_result_combine": (C.c_int, [_P, C.c_int, _P, _P]),
     "smap_volume": (C.c_uint64, [C.c_int, C.c_int64, C.c_int]),
     "smap_locate": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
     "smap_destroy": (None, [_P]),
@@ -228,6 +229,13 @@ def smap_result_reduce(plan: Plan, dst, stream=None):
     _check(_lib.smap_result_reduce(plan.handle, _ptr(dst), _stream(stream)))
 
 
+def smap_result_combine(records, count: int, dst, stream=None):
+    """Asynchronously combine `count` device records (7 int64 each, contiguous)
+    into `dst` (7 int64 on the device): the cross-rank step after an
+    all-gather of every rank's smap_result_reduce output, in one kernel."""
+    _check(_lib.smap_result_combine(_ptr(records), int(count), _ptr(dst), _stream(stream)))
+
+
 def result_dict(rec) -> dict:
     """Host view of a 6 x int64 result record."""
     import numpy as np
@@ -267,5 +275,6 @@ def alloc_out(plan: Plan, payload: str, device="cuda", zero: bool = False):
 
 
 __all__ = ["smap_plan", "smap_plan_query", "smap_out_bytes", "smap_run", "smap_run_host", "smap_stats_fetch",
+           "smap_result_reduce", "smap_result_combine",
            "smap_volume", "smap_destroy", "smap_last_error", "smap_abi_version", "Plan", "SmapError",
            "alloc_out", "exported_symbols", "RUN_CHECKSUM", "RUN_CHECKSUM_MIX", "RUN_XOR"]

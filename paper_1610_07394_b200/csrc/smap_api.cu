@@ -114,6 +114,10 @@ static uint64_t below_pieces(int m, int64_t M, std::vector<Piece> &out)
     return start;
 }
 
+namespace smap {
+__global__ void k_result_combine(const smap_result *recs, int G, smap_result *dst);
+}
+
 extern "C" {
 
 int smap_abi_version(void) { return SMAP_ABI_VERSION; }
@@ -531,6 +535,20 @@ smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream)
     return SMAP_OK;
 }
 
+smap_status smap_result_combine(const void *records, int count, void *dst, void *stream)
+{
+    g_err.clear();
+    if (!records || !dst) return fail(SMAP_E_INVALID, "smap_result_combine: NULL argument");
+    if (count < 1) return fail(SMAP_E_INVALID, "smap_result_combine: count must be >= 1 (got %d)", count);
+    if (((reinterpret_cast<uintptr_t>(records) | reinterpret_cast<uintptr_t>(dst)) & 7) != 0)
+        return fail(SMAP_E_INVALID, "smap_result_combine: pointers must be 8-byte aligned");
+    k_result_combine<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<const smap_result *>(records), count,
+                                                          reinterpret_cast<smap_result *>(dst));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "result combine launch");
+    return SMAP_OK;
+}
+
 smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, float param, void *out,
                           size_t out_bytes, uint32_t flags, void *stream, smap_stats *stats)
 {
@@ -627,6 +645,30 @@ __global__ void __launch_bounds__(32) k_result_reduce(const Result *res, smap_re
         dst->count = v[0]; dst->s0 = v[1]; dst->s1 = v[2]; dst->mix = v[3]; dst->tc = v[4];
         dst->xr = xr;
         dst->sum = res->sum;
+    }
+}
+
+// Combine G device records in one warp: integer fields add mod 2^64, xr by
+// xor, the fp64 sums in record order 0, 1, ..., G-1 (deterministic).
+__global__ void __launch_bounds__(32) k_result_combine(const smap_result *recs, int G, smap_result *dst)
+{
+    const int lane = threadIdx.x;
+    uint64_t v[5] = {0, 0, 0, 0, 0}, xr = 0;
+    for (int g = lane; g < G; g += 32) {
+        const smap_result r = recs[g];
+        v[0] += r.count; v[1] += r.s0; v[2] += r.s1; v[3] += r.mix; v[4] += r.tc;
+        xr ^= r.xr;
+    }
+#pragma unroll
+    for (int k = 0; k < 5; k++) v[k] = warp_sum_u64(v[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xr ^= __shfl_xor_sync(0xffffffffu, xr, o);
+    if (lane == 0) {
+        double sum = 0.0;
+        for (int g = 0; g < G; g++) sum += recs[g].sum;
+        dst->count = v[0]; dst->s0 = v[1]; dst->s1 = v[2]; dst->mix = v[3]; dst->tc = v[4];
+        dst->xr = xr;
+        dst->sum = sum;
     }
 }
 

@@ -339,3 +339,26 @@ def test_tile64_m3(sm, orc, map_):
         assert st["tc"] == orc.tc_count(p, np.float32(R))
     with pytest.raises(sm.SmapError):
         sm.smap_run(plan, "atm", points=dev_points(p), param=1e-2)
+
+
+@pytest.mark.parametrize("G", [1, 2, 8, 33])
+def test_result_combine_kernel(sm, G):
+    """smap_result_combine (the bench's cross-rank step after the all-gather)
+    equals the plain combination: integer fields mod 2^64, xor, fp64 sums in
+    record order."""
+    import bench
+    rng = np.random.default_rng(G)
+    recs = rng.integers(-(1 << 63), (1 << 63) - 1, size=(G, 7), dtype=np.int64)
+    recs[:, 6] = rng.standard_normal(G).view(np.int64)
+    d = torch.from_numpy(recs).cuda()
+    out = torch.zeros(7, dtype=torch.int64, device="cuda")
+    sm.smap_result_combine(d, G, out)
+    exp = bench.combine_records(torch.from_numpy(recs))
+    got = out.cpu()
+    assert torch.equal(got[:6], exp[:6])
+    s = 0.0
+    for g in range(G):
+        s += float(recs[g, 6:7].view(np.float64)[0])
+    assert float(got[6:7].numpy().view(np.float64)[0]) == s
+    sm.smap_result_combine(d, G, d[0])                  # dst may alias records[0]
+    assert torch.equal(d[0].cpu()[:6], exp[:6])
