@@ -357,9 +357,8 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     CK(cudaGetDevice(&cur));
     if (cur != p->device) CK(cudaSetDevice(p->device));
     const bool tc_bits = ipl == PL_TC && tile;
-    const int64_t npad = (int64_t)p->P.N * d.rho;          // bitmap over the padded index range
-    if (tc_bits && (npad % 32) != 0) return fail(SMAP_E_UNSUPPORTED, "bit-sliced TC needs 2^ceil(log2 n) >= 32");
-    if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)npad * (size_t)(npad / 32) * sizeof(uint32_t)));
+    const int64_t npad = (int64_t)p->P.N * d.rho;          // bitmap over the grid's index range
+    if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)npad * (size_t)((npad + 31) / 32) * sizeof(uint32_t)));
     if (atm) {
         const uint64_t np = tile ? p->ctas : p->P.nblocks;
         if (np > p->npartials) {

@@ -139,9 +139,9 @@ cudaError_t launch_thread2(const Params &P, int map, bool incl, int pl, int cs, 
 cudaError_t launch_thread3(const Params &P, int map, int pl, int cs, cudaStream_t s);
 cudaError_t launch_tile2(const Params &P, int T, int map, bool incl, int pl, int cs, unsigned ctas, cudaStream_t s);
 cudaError_t launch_tile3(const Params &P, int T, int map, int pl, int cs, unsigned ctas, cudaStream_t s);
-// TC pre-pass: adj[j * (npad/32) + w] bit b <=> 32w + b < n, j < n and
+// TC pre-pass: adj[j * ceil(npad/32) + w] bit b <=> 32w + b < n, j < n and
 // r2(32w + b, j) < R*R (the same fp32 predicate as the per-triple compare);
-// npad = N * rho, a multiple of 32.
+// npad = N * rho (rows j < npad, words rounded up).
 cudaError_t launch_tc_adjacency(const float *pts, int n, int npad, float R, uint32_t *adj, cudaStream_t s);
 // Deterministic fixed-order fp64 reduction of partials[0..np) into res->sum.
 // Adds the number of kernels it launched to *launches.

@@ -1,0 +1,52 @@
+"""One small run of every kernel family (for compute-sanitizer memcheck /
+racecheck / synccheck on the GPU box):
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_cases.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+import paper_1610_07394_b200 as sm
+import workloads
+
+
+def main():
+    p2 = torch.from_numpy(workloads.points(1000, 1)).cuda()
+    p3 = torch.from_numpy(workloads.points(300, 2)).cuda()
+    runs = 0
+    for mp in ("lambda", "bb", "below", "enum"):
+        for gran, rho2, rho3 in (("thread", 16, 8), ("tile", 64, 16), ("tile", 128, 32)):
+            if (mp == "below" and gran == "thread") or (mp == "enum" and gran == "tile"):
+                continue
+            for m, n, rho, pts in ((2, 1000, rho2, p2), (3, 300, rho3, p3)):
+                for diag in ("strict", "inclusive"):
+                    plan = sm.smap_plan(m, n, rho, map=mp, diag=diag, granularity=gran)
+                    pls = ["index_write", "hitcount", "map_dump", "empty"]
+                    if diag == "strict":
+                        pls += ["edm"] if m == 2 else ["atm", "tc", "index_write_atm"]
+                    for pl in pls:
+                        out = sm.alloc_out(plan, pl, zero=True)
+                        sm.smap_run(plan, pl, points=pts, param=0.5 if pl == "tc" else 1e-2, out=out,
+                                    flags=sm.RUN_CHECKSUM_MIX if pl in ("index_write", "edm", "index_write_atm") else 0)
+                        sm.smap_stats_fetch(plan)
+                        runs += 1
+    # tile layouts, sharded
+    for m, n, rho in ((2, 1024, 64), (3, 256, 16), (3, 256, 32)):
+        pts = torch.from_numpy(workloads.points(n, 3)).cuda()
+        for r in range(2):
+            plan = sm.smap_plan(m, n, rho, granularity="tile", layout="tiles", shard_rank=r, shard_count=2)
+            for pl in ("index_write",) + (("edm",) if m == 2 else ("index_write_atm",)):
+                out = sm.alloc_out(plan, pl)
+                sm.smap_run(plan, pl, points=pts, param=1e-2, out=out, flags=sm.RUN_XOR)
+                sm.smap_stats_fetch(plan)
+                runs += 1
+    torch.cuda.synchronize()
+    print(f"sanitize cases: {runs} runs ok")
+
+
+if __name__ == "__main__":
+    main()

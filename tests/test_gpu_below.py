@@ -78,7 +78,7 @@ def test_edm_bit_exact(sm, orc, n, T):
             assert (st["count"], st["s0"], st["s1"]) == (cs["count"], cs["s0"], cs["s1"])
 
 
-@pytest.mark.parametrize("n,T", [(300, 8), (300, 16), (333, 32), (250, 32)])
+@pytest.mark.parametrize("n,T", [(300, 8), (300, 16), (333, 32), (250, 32), (20, 8), (45, 16)])
 def test_atm_tc_iwa(sm, orc, n, T):
     p = workloads.points(n, workloads.SEED_C3)
     dp = dev(p)
@@ -91,10 +91,17 @@ def test_atm_tc_iwa(sm, orc, n, T):
     out, st = run(sm, plan, "index_write_atm", points=dp, param=1e-2, flags=sm.RUN_XOR)
     assert st["count"] == V and abs(st["sum"] - ref) <= 1e-5 * abs(ref)
     np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), np.arange(V, dtype=np.uint32))
-    if (-(-n // T) * T) % 32 == 0:                      # the bit-sliced TC bitmap needs M*T % 32 == 0
-        for R in (0.5, 0.2):
-            _, st = run(sm, plan, "tc", points=dp, param=R)
-            assert st["tc"] == orc.tc_count(p, np.float32(R)) and st["count"] == V
+    for R in (0.5, 0.2):                                # (M*T need not be a multiple of 32)
+        _, st = run(sm, plan, "tc", points=dp, param=R)
+        assert st["tc"] == orc.tc_count(p, np.float32(R)) and st["count"] == V
+
+
+@pytest.mark.parametrize("n", [100, 700, 2100])
+def test_tc_tile64(sm, orc, n):
+    p = workloads.points(n, workloads.SEED_C5)
+    plan = sm.smap_plan(3, n, 64, map="below", granularity="tile", persistent=8)
+    _, st = run(sm, plan, "tc", points=dev(p), param=0.5)
+    assert st["tc"] == orc.tc_count(p, np.float32(0.5)) and st["count"] == math.comb(n, 3)
 
 
 def test_below_vs_above_full_size(sm, orc):
