@@ -63,7 +63,10 @@ typedef enum {
                                 simplex mapped by lambda (lambda2 inclusive tile grid, lambda3 for
                                 N_s >= 8) or a box / small simplex at the identity, so every launched
                                 tile holds elements (besides lambda3's own idle tiles).  Any n; TILE
-                                granularity, canonical layout, unsharded. */
+                                granularity, unsharded.  With SMAP_LAYOUT_TILES (reading E29) every
+                                tile is one slot in launch order whose size depends on its class only
+                                (T^m, diagonal/face, body); elements of a tile cut by n leave holes,
+                                so smap_out_bytes may exceed V * sizeof(element); no smap_locate. */
 } smap_map;
 
 typedef enum {
@@ -240,7 +243,7 @@ smap_status smap_result_combine(const void *records, int count, void *dst, void 
  * SMAP_LAYOUT_TILES: the position in the shard-local tile-blocked array).
  * Host only, O(1) (lambda2^-1 via b = 2^floor(log2(I xor J)), q = I >> (log2 b + 1)).
  * SMAP_E_INVALID for an element outside the domain; SMAP_E_UNSUPPORTED for m=3 with
- * shard_count > 1. */
+ * shard_count > 1 and for BELOW plans with the tile-blocked layout. */
 smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *pos);
 
 /* Useful-element count V of a domain: C(n,2), n(n+1)/2 or C(n,3).  Host only. */

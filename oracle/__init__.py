@@ -85,6 +85,8 @@ _SIGS = {
     "or_below_segments": (i32, [u64, P, P]),
     "or_below_tiles": (u64, [i32, u64, P]),
     "or_below_element_hits": (i32, [i32, i32, u64, u64, P, u64, P]),
+    "or_below_tile_layout": (i64, [i32, i32, u64, u64, P, u64]),
+    "or_cs_below_tiles": (i32, [i32, i32, i32, u64, u64, P, i32, P]),
 }
 
 
@@ -382,3 +384,21 @@ def below_element_hits(m, inclusive, n, T):
     res = np.zeros(3, np.int64)
     assert lib().or_below_element_hits(m, int(inclusive), n, T, _ptr(hits), V, _ptr(res)) == 0
     return hits, dict(zip(("tiles", "useful", "outside"), (int(x) for x in res)))
+
+
+def below_tile_layout(m, inclusive, n, T):
+    """(pos_of_rank, layout length incl. holes) of the E29 tile-blocked layout."""
+    V = domain_volume(m, inclusive, n)
+    pos = np.zeros(V, np.int64)
+    L = lib().or_below_tile_layout(m, int(inclusive), n, T, _ptr(pos), V)
+    assert L >= 0
+    return pos, int(L)
+
+
+def cs_below_tiles(payload, m, inclusive, n, T, points=None, nthreads=0):
+    """Streaming checksum of index write (payload "index_write") or EDM in the E29 layout."""
+    cs = np.zeros(5, np.uint64)
+    pts = _pts(points) if points is not None else np.zeros((1, 3), np.float32)
+    assert lib().or_cs_below_tiles(1 if payload == "edm" else 0, m, int(inclusive), n, T, _ptr(pts), nthreads,
+                                   _ptr(cs)) == 0
+    return dict(zip(CS_KEYS, (int(v) for v in cs)))

@@ -1313,3 +1313,124 @@ int or_below_element_hits(int m, int inclusive, uint64_t n, uint64_t T, uint32_t
     res[0] = (int64_t)nt; res[1] = useful; res[2] = outside;
     return 0;
 }
+
+/* ======================================================================
+ * Tile-blocked layout of the below decomposition (reading E29): the tiles
+ * in the launch order of or_below_tiles, each one contiguous slot holding its
+ * elements in the kernel's row order -- m=2 rows r then columns c (diagonal
+ * tiles clipped to c < r / c <= r); m=3 the segments of E26 (k_l, j_l, i_l).
+ * Slot sizes ignore the cut by n: an element whose largest index is >= n'
+ * keeps its position as a hole (never written), so every slot size depends on
+ * the tile class only.  pos_of_rank[p] = position of packed rank p.
+ * ====================================================================== */
+static uint64_t or_below_slot_size(int m, int inclusive, const int32_t *r, uint64_t T)
+{
+    if (m == 2) return r[3] == 2 ? (inclusive ? T * (T + 1) / 2 : T * (T - 1) / 2) : T * T;
+    if (r[3] == 3) return 0;
+    if (r[3] == 2) return T * (T - 1) * (T - 2) / 6;
+    if (r[3] == 5 || r[3] == 6) return T * T * (T - 1) / 2;
+    if (r[0] == r[1]) return T * T * (T - 1);              /* lambda3 face tile: both segments */
+    return T * T * T;
+}
+
+/* calls BODY with (pos, rank) for every element of record r, positions from pos */
+#define OR_BELOW_WALK(m, inclusive, nint, r, T, POS, BODY)                                              \
+    do {                                                                                                \
+        if ((m) == 2) {                                                                                 \
+            uint64_t J_ = (uint64_t)(r)[0], I_ = (uint64_t)(r)[1];                                      \
+            for (uint64_t rr = 0; rr < (T); rr++)                                                       \
+                for (uint64_t cc = 0; cc < (T); cc++) {                                                 \
+                    if ((r)[3] == 2 && ((inclusive) ? cc > rr : cc >= rr)) continue;                    \
+                    uint64_t i_ = I_ * (T) + rr, j_ = J_ * (T) + cc;                                    \
+                    if (i_ < (nint)) {                                                                  \
+                        uint64_t rank_ = (inclusive) ? or_rank2_incl(i_, j_) : or_rank2_strict(i_, j_); \
+                        BODY;                                                                           \
+                    }                                                                                   \
+                    (POS)++;                                                                            \
+                }                                                                                       \
+        } else if ((r)[3] != 3) {                                                                       \
+            uint64_t I_ = (uint64_t)(r)[0], J_ = (uint64_t)(r)[1], K_ = (uint64_t)(r)[2];              \
+            or_seg3 sg_[2];                                                                             \
+            int ns_ = 1;                                                                                \
+            if ((r)[3] == 2) { sg_[0].I = sg_[0].J = sg_[0].K = I_; sg_[0].kind = 3; }                  \
+            else if (I_ < J_ && J_ < K_) { sg_[0].I = I_; sg_[0].J = J_; sg_[0].K = K_; sg_[0].kind = 0; } \
+            else if ((r)[3] == 5) { sg_[0].I = I_; sg_[0].J = I_; sg_[0].K = K_; sg_[0].kind = 1; }    \
+            else if ((r)[3] == 6) { sg_[0].I = I_; sg_[0].J = K_; sg_[0].K = K_; sg_[0].kind = 2; }    \
+            else {                                                                                      \
+                sg_[0].I = I_; sg_[0].J = I_; sg_[0].K = K_; sg_[0].kind = 1;                           \
+                sg_[1].I = I_; sg_[1].J = K_; sg_[1].K = K_; sg_[1].kind = 2; ns_ = 2;                  \
+            }                                                                                           \
+            for (int q_ = 0; q_ < ns_; q_++)                                                            \
+                for (uint64_t kl = 0; kl < (T); kl++)                                                   \
+                    for (uint64_t jl = 0; jl < (T); jl++) {                                             \
+                        if ((sg_[q_].kind == 2 || sg_[q_].kind == 3) && jl >= kl) continue;             \
+                        for (uint64_t il = 0; il < (T); il++) {                                         \
+                            if ((sg_[q_].kind == 1 || sg_[q_].kind == 3) && il >= jl) continue;         \
+                            uint64_t i_ = sg_[q_].I * (T) + il, j_ = sg_[q_].J * (T) + jl, k_ = sg_[q_].K * (T) + kl; \
+                            if (k_ < (nint)) {                                                          \
+                                uint64_t rank_ = (inclusive) ? or_rank3_incl(i_, j_ - 1, k_ - 2) : or_rank3(i_, j_, k_); \
+                                BODY;                                                                   \
+                            }                                                                           \
+                            (POS)++;                                                                    \
+                        }                                                                               \
+                    }                                                                                   \
+        }                                                                                               \
+    } while (0)
+
+/* returns the layout length (slots incl. holes), or -1 */
+int64_t or_below_tile_layout(int m, int inclusive, uint64_t n, uint64_t T, int64_t *pos_of_rank, uint64_t V)
+{
+    uint64_t nint = (m == 3 && inclusive) ? n + 2 : n;
+    uint64_t M = (nint + T - 1) / T, nt = or_below_tiles(m, M, NULL);
+    int32_t *rec = malloc(nt * 4 * sizeof(int32_t));
+    if (!rec) return -1;
+    or_below_tiles(m, M, rec);
+    for (uint64_t p = 0; p < V; p++) pos_of_rank[p] = -1;
+    uint64_t pos = 0;
+    int bad = 0;
+    for (uint64_t t = 0; t < nt; t++) {
+        const int32_t *r = rec + 4 * t;
+        uint64_t p0 = pos;
+        OR_BELOW_WALK(m, inclusive, nint, r, T, pos, {
+            if (rank_ >= V) bad = 1; else pos_of_rank[rank_] = (int64_t)pos;
+        });
+        if (pos - p0 != or_below_slot_size(m, inclusive, r, T)) bad = 1;
+    }
+    free(rec);
+    return bad ? -1 : (int64_t)pos;
+}
+
+/* Streaming checksum (E21) of a payload written in the E29 layout: index
+ * write (payload 0, value = packed rank) or EDM (payload 1, m=2 strict). */
+int or_cs_below_tiles(int payload, int m, int inclusive, uint64_t n, uint64_t T, const float *pts, int nthreads,
+                      uint64_t *cs)
+{
+    uint64_t nint = (m == 3 && inclusive) ? n + 2 : n;
+    uint64_t M = (nint + T - 1) / T, nt = or_below_tiles(m, M, NULL);
+    int32_t *rec = malloc(nt * 4 * sizeof(int32_t));
+    uint64_t *off = malloc((nt + 1) * sizeof(uint64_t));
+    if (!rec || !off) { free(rec); free(off); return -1; }
+    or_below_tiles(m, M, rec);
+    off[0] = 0;
+    for (uint64_t t = 0; t < nt; t++) off[t + 1] = off[t] + or_below_slot_size(m, inclusive, rec + 4 * t, T);
+    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+    int ntr = or_threads(nthreads);
+    #pragma omp parallel for schedule(dynamic, 4) reduction(+:c0,c1,c2,c3) reduction(^:c4) num_threads(ntr)
+    for (uint64_t t = 0; t < nt; t++) {
+        uint64_t c[5] = {0, 0, 0, 0, 0};
+        const int32_t *r = rec + 4 * t;
+        uint64_t pos = off[t];
+        if (payload == 1 && m == 2) {
+            OR_BELOW_WALK(2, inclusive, nint, r, T, pos, {
+                (void)rank_;
+                or_cs_add(c, pos, or_fbits(or_edm_dist(pts, i_, j_)));
+            });
+        } else {
+            OR_BELOW_WALK(m, inclusive, nint, r, T, pos, { or_cs_add(c, pos, rank_); });
+        }
+        c0 += c[0]; c1 += c[1]; c2 += c[2]; c3 += c[3]; c4 ^= c[4];
+    }
+    free(rec); free(off);
+    cs[0] = c0; cs[1] = c1; cs[2] = c2; cs[3] = c3; cs[4] = c4;
+    return 0;
+}

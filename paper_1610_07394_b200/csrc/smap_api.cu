@@ -31,6 +31,7 @@ struct smap_plan_s {
     double *d_scratch = nullptr;
     uint32_t *d_adj = nullptr;      // TC pair-predicate bitmap (TILE)
     Piece *d_pieces = nullptr;      // SMAP_MAP_BELOW decomposition
+    uint64_t layout_len = 0;        // SMAP_MAP_BELOW tile-blocked layout: slots incl. holes (E29)
     std::vector<Piece> pieces;
     float *d_stage = nullptr;
     smap_result *d_rec = nullptr;   // smap_run_host: device record
@@ -71,7 +72,7 @@ static int ilog2(int64_t x) { int l = 0; while ((int64_t)1 << (l + 1) <= x) l++;
 
 // "Approach n from below" (reading E28): the pieces of the M-tile
 // simplex in launch order (include/smap.h); returns the total tile count.
-static uint64_t below_pieces(int m, int64_t M, std::vector<Piece> &out)
+static uint64_t below_pieces(int m, int64_t M, int T, bool incl, std::vector<Piece> &out, uint64_t *slots)
 {
     std::vector<uint32_t> Ns, Os;
     for (int64_t rest = M, off = 0; rest > 0;) {        // binary digits of M, largest first
@@ -81,37 +82,46 @@ static uint64_t below_pieces(int m, int64_t M, std::vector<Piece> &out)
     }
     const int p = (int)Ns.size();
     uint64_t start = 0;
-    auto add = [&](uint8_t kind, int a, int b, int c, uint64_t count) {
+    uint64_t sbase = 0;
+    auto add = [&](uint8_t kind, int a, int b, int c, uint64_t count, uint64_t slots) {
         Piece pc;
-        pc.start = start; pc.kind = kind;
+        pc.start = start; pc.kind = kind; pc.sbase = sbase;
+        sbase += slots;
         pc.Oa = Os[a]; pc.Ob = Os[b]; pc.Oc = Os[c];
         pc.ea = (uint8_t)ilog2(Ns[a]); pc.eb = (uint8_t)ilog2(Ns[b]); pc.ec = (uint8_t)ilog2(Ns[c]);
         out.push_back(pc);
         start += count;
     };
     auto tri = [](uint64_t N) { return N == 1 ? (uint64_t)1 : (N / 2) * (N + 1); };   // lambda2 inclusive tile grid
+    // E29 slot totals: a triangle piece holds N diagonal tiles (size sd) and (N/2)(N-1) full ones
+    auto tri_slots = [](uint64_t N, uint64_t sd, uint64_t sf) { return N * sd + (N / 2) * (N - 1) * sf; };
+    const uint64_t T2 = (uint64_t)T * T, T3 = T2 * T, Tf = T2 * (T - 1) / 2, Tb = (uint64_t)T * (T - 1) * (T - 2) / 6;
     if (m == 2) {
+        const uint64_t sd = incl ? (uint64_t)T * (T + 1) / 2 : (uint64_t)T * (T - 1) / 2;
         for (int s = 0; s < p; s++) {
-            add(PK_TRI2, s, s, s, tri(Ns[s]));
-            for (int a = 0; a < s; a++) add(PK_RECT2, a, s, s, (uint64_t)Ns[a] * Ns[s]);
+            add(PK_TRI2, s, s, s, tri(Ns[s]), tri_slots(Ns[s], sd, T2));
+            for (int a = 0; a < s; a++) add(PK_RECT2, a, s, s, (uint64_t)Ns[a] * Ns[s], (uint64_t)Ns[a] * Ns[s] * T2);
         }
+        *slots = sbase;
         return start;
     }
     for (int c = 0; c < p; c++)
         for (int b = 0; b <= c; b++)
             for (int a = 0; a <= b; a++) {
                 const uint64_t Na = Ns[a], Nb = Ns[b], Nc = Ns[c];
-                if (a == c) {
-                    if (Na >= 8) add(PK_TET3, a, a, a, (Na / 2) * (Na / 2) * (3 * Na / 4));
-                    else add(PK_TETS, a, a, a, Na * (Na + 1) * (Na + 2) / 6);
+                if (a == c) {                 // interior C(N,3) T^3 + faces C(N,2) T^2(T-1) + bodies N C(T,3)
+                    const uint64_t sl = Na * (Na - 1) * (Na - 2) / 6 * T3 + Na * (Na - 1) / 2 * 2 * Tf + Na * Tb;
+                    if (Na >= 8) add(PK_TET3, a, a, a, (Na / 2) * (Na / 2) * (3 * Na / 4), sl);
+                    else add(PK_TETS, a, a, a, Na * (Na + 1) * (Na + 2) / 6, sl);
                 } else if (b == c) {
-                    add(PK_LT, a, b, c, Na * tri(Nb));
+                    add(PK_LT, a, b, c, Na * tri(Nb), Na * tri_slots(Nb, Tf, T3));
                 } else if (a == b) {
-                    add(PK_TL, a, b, c, Nc * tri(Na));
+                    add(PK_TL, a, b, c, Nc * tri(Na), Nc * tri_slots(Na, Tf, T3));
                 } else {
-                    add(PK_BOX, a, b, c, Na * Nb * Nc);
+                    add(PK_BOX, a, b, c, Na * Nb * Nc, Na * Nb * Nc * T3);
                 }
             }
+    *slots = sbase;
     return start;
 }
 
@@ -154,7 +164,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     const bool below = d->map == SMAP_MAP_BELOW;
     if (enm && tile) return fail(SMAP_E_INVALID, "the enumeration baseline map is THREAD granularity only");
     if (below && !tile) return fail(SMAP_E_INVALID, "the approach-from-below map is TILE granularity only");
-    if (below && d->layout != SMAP_LAYOUT_ROWS) return fail(SMAP_E_UNSUPPORTED, "the approach-from-below map writes the canonical layout");
+
     if (d->diag != SMAP_DIAG_STRICT && d->diag != SMAP_DIAG_INCLUSIVE) return fail(SMAP_E_INVALID, "bad diag %d", d->diag);
     if (d->granularity != SMAP_GRAN_THREAD && d->granularity != SMAP_GRAN_TILE)
         return fail(SMAP_E_INVALID, "bad granularity %d", d->granularity);
@@ -193,7 +203,8 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (d->layout == SMAP_LAYOUT_TILES && m == 3 && incl)
         return fail(SMAP_E_UNSUPPORTED, "the m=3 tile-blocked layout is for the strict diagonal");
     if (padded && G != 1) return fail(SMAP_E_UNSUPPORTED, "sharding needs n to be a power of two (padded grids are not volume-balanced)");
-    if (padded && d->layout == SMAP_LAYOUT_TILES) return fail(SMAP_E_UNSUPPORTED, "the tile-blocked layout needs n to be a power of two");
+    if (padded && !below && d->layout == SMAP_LAYOUT_TILES)
+        return fail(SMAP_E_UNSUPPORTED, "the lambda/BB tile-blocked layout needs n to be a power of two (BELOW: any n)");
 
     smap_plan_s *p = new (std::nothrow) smap_plan_s();
     if (!p) return fail(SMAP_E_NOMEM, "host allocation failed");
@@ -206,7 +217,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
         const int64_t M = (nint + rho - 1) / rho;
         P.N = (int)M; P.log2N = 0;
         P.W = (int)M; P.log2W = 0; P.wx0 = 0;
-        P.nblocks = below_pieces(m, M, p->pieces);
+        P.nblocks = below_pieces(m, M, rho, incl, p->pieces, &p->layout_len);
         P.npieces = (int)p->pieces.size();
     } else if (lam) {
         P.W = (int)(N / 2 / G); P.log2W = ilog2(P.W); P.wx0 = d->shard_rank * P.W;
@@ -303,7 +314,9 @@ static int internal_pl(smap_plan_t p, smap_payload pl)
 smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes)
 {
     if (!p || !bytes) return fail(SMAP_E_INVALID, "smap_out_bytes: NULL argument");
-    const uint64_t Vout = p->d.layout == SMAP_LAYOUT_TILES ? p->useful : p->V;   // tile layout: shard-local
+    // tile layout: shard-local; BELOW: the slots incl. the holes of tiles cut by n (E29)
+    const uint64_t Vout = p->d.layout != SMAP_LAYOUT_TILES ? p->V
+                        : p->d.map == SMAP_MAP_BELOW ? p->layout_len : p->useful;
     switch (pl) {
     case SMAP_PAYLOAD_INDEX_WRITE:
     case SMAP_PAYLOAD_INDEX_WRITE_ATM: *bytes = (size_t)Vout * (p->elem64 ? 8 : 4); break;
@@ -434,6 +447,8 @@ smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *p
 {
     if (!p || !e || !shard || !pos) return fail(SMAP_E_INVALID, "smap_locate: NULL argument");
     const smap_plan_desc &d = p->d;
+    if (d.map == SMAP_MAP_BELOW && d.layout == SMAP_LAYOUT_TILES)
+        return fail(SMAP_E_UNSUPPORTED, "smap_locate: no O(1) inverse for the approach-from-below tile layout");
     const bool lam = d.map == SMAP_MAP_LAMBDA, incl = d.diag == SMAP_DIAG_INCLUSIVE;
     const int64_t n = d.n;
     if (d.m == 3) {

@@ -38,6 +38,7 @@ enum PieceKind {
 };
 struct Piece {
     uint64_t start;            // first tile id of the piece (launch order)
+    uint64_t sbase;            // first position of the piece in the tile-blocked layout (E29)
     uint32_t Oa, Ob, Oc;       // segment offsets (tiles)
     uint8_t kind, ea, eb, ec;  // PieceKind, log2 of the segment sizes
 };

@@ -37,7 +37,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     a = ap.parse_args()
     rows = []
-    cases = [(2, 40000, "edm", 128, workloads.SEED_C2, 0.0), (2, 70000, "edm", 128, workloads.SEED_C2, 0.0),
+    cases = [(2, 40000, "edm", 256, workloads.SEED_C2, 0.0), (2, 70000, "edm", 256, workloads.SEED_C2, 0.0),
              (2, 100000, "index_write", 128, None, 0.0),
              (3, 1100, "index_write", 32, None, 0.0), (3, 1100, "atm", 32, workloads.SEED_C3, 1e-2),
              (3, 1500, "atm", 32, workloads.SEED_C3, 1e-2), (3, 2100, "tc", 64, workloads.SEED_C5, 0.5),
@@ -46,7 +46,17 @@ def main():
         pts = torch.from_numpy(workloads.points(n, seed)).cuda() if seed else None
         row = {"m": m, "n": n, "payload": payload, "tile": T, "elements": sm.smap_volume(m, n)}
         out = None
-        for mp in ("below", "lambda", "bb"):
+        for mp in ("below", "below_tiles", "lambda", "bb"):
+            if mp == "below_tiles":
+                if payload not in ("edm", "index_write"):
+                    continue
+                plan = sm.smap_plan(m, n, T, map="below", granularity="tile", layout="tiles")
+                tout = sm.alloc_out(plan, payload)
+                ms = med(plan, payload, pts, param, tout, sm.RUN_XOR, a.reps)
+                st = sm.smap_stats_fetch(plan)
+                row[mp] = {"ms": round(ms, 4), "count": st["count"]}
+                del tout
+                continue
             plan = sm.smap_plan(m, n, T, map=mp, granularity="tile")
             if out is None:
                 out = sm.alloc_out(plan, payload)

@@ -117,3 +117,71 @@ def test_below_vs_above_full_size(sm, orc):
         assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"]), mp
         del out
         torch.cuda.empty_cache()
+
+
+SENT = 0x7FABCDEF
+
+
+@pytest.mark.parametrize("m,n,T", [(2, 1000, 32), (2, 1500, 128), (2, 777, 512), (2, 1024, 64), (3, 300, 8),
+                                   (3, 300, 16), (3, 333, 32), (3, 256, 32), (3, 200, 64)])
+@pytest.mark.parametrize("diag", ["strict", "inclusive"])
+def test_tile_layout_index_write(sm, orc, m, n, T, diag):
+    """E29: every packed rank lands at the oracle's position and the holes of
+    tiles cut by n are never written."""
+    if m == 3 and diag == "inclusive":
+        pytest.skip("the m=3 tile-blocked layout is for the strict diagonal")
+    plan = sm.smap_plan(m, n, T, map="below", diag=diag, granularity="tile", layout="tiles")
+    pos, L = orc.below_tile_layout(m, diag == "inclusive", n, T)
+    out = sm.alloc_out(plan, "index_write")
+    assert out.numel() == L
+    out.fill_(SENT)
+    sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM_MIX)
+    st = sm.smap_stats_fetch(plan)
+    got = out.cpu().numpy().view(np.uint32)
+    V = len(pos)
+    np.testing.assert_array_equal(got[pos], np.arange(V, dtype=np.uint32))
+    holes = np.ones(L, bool)
+    holes[pos] = False
+    assert (got[holes] == SENT).all()
+    cs = orc.cs_below_tiles("index_write", m, diag == "inclusive", n, T)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+
+
+@pytest.mark.parametrize("n,T", [(1500, 64), (3001, 128), (5000, 256), (4096, 128)])
+def test_tile_layout_edm(sm, orc, n, T):
+    p = workloads.points(n, workloads.SEED_C2)
+    plan = sm.smap_plan(2, n, T, map="below", granularity="tile", layout="tiles")
+    pos, L = orc.below_tile_layout(2, False, n, T)
+    exp = orc.edm(p)
+    for flags in (0, sm.RUN_XOR, sm.RUN_CHECKSUM):
+        out, st = run(sm, plan, "edm", points=dev(p), flags=flags)
+        got = out.cpu().numpy().view(np.uint32)
+        np.testing.assert_array_equal(got[pos], exp.view(np.uint32))
+        if flags:
+            cs = orc.cs_below_tiles("edm", 2, False, n, T, points=p)
+            assert st["count"] == cs["count"]
+            assert (st["xr"] if flags == sm.RUN_XOR else st["s1"]) == (cs["xr"] if flags == sm.RUN_XOR else cs["s1"])
+
+
+@pytest.mark.parametrize("n,T", [(300, 16), (333, 32), (1100, 32)])
+def test_tile_layout_fused_iwa(sm, orc, n, T):
+    p = workloads.points(n, workloads.SEED_C3)
+    plan = sm.smap_plan(3, n, T, map="below", granularity="tile", layout="tiles")
+    out, st = run(sm, plan, "index_write_atm", points=dev(p), param=1e-2, flags=sm.RUN_CHECKSUM_MIX)
+    cs = orc.cs_below_tiles("index_write", 3, False, n, T)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+    ref = orc.atm_sum(p, np.float32(1e-2))
+    assert abs(st["sum"] - ref) <= 1e-5 * abs(ref)
+
+
+def test_tile_layout_edm_full_size(sm, orc):
+    """n = 70000 EDM (2.45e9 pairs) in the E29 layout: streaming checksums of
+    the whole output against the oracle's walk of the same layout."""
+    n = 70000
+    p = workloads.points(n, workloads.SEED_C2)
+    plan = sm.smap_plan(2, n, 128, map="below", granularity="tile", layout="tiles")
+    out, st = run(sm, plan, "edm", points=dev(p), flags=sm.RUN_CHECKSUM_MIX)
+    cs = orc.cs_below_tiles("edm", 2, False, n, 128, points=p)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+    del out
+    torch.cuda.empty_cache()

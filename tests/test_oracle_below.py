@@ -128,5 +128,48 @@ def test_host_plan_rejects(orc):
         sm.smap_plan(2, 1000, 16, map="below", device=N)                      # THREAD granularity
     with pytest.raises(sm.SmapError):
         sm.smap_plan(2, 1000, 32, map="below", granularity="tile", shard_count=2, device=N)
-    with pytest.raises(sm.SmapError):
-        sm.smap_plan(2, 1024, 32, map="below", granularity="tile", layout="tiles", device=N)
+    with pytest.raises(sm.SmapError):                                        # m=3 inclusive tile layout
+        sm.smap_plan(3, 1000, 32, map="below", diag="inclusive", granularity="tile", layout="tiles", device=N)
+
+
+@pytest.mark.parametrize("m,inc,n,T", [(2, False, 100, 8), (2, True, 37, 4), (2, False, 64, 8), (2, False, 1000, 32),
+                                       (3, False, 100, 8), (3, False, 64, 8), (3, False, 37, 4), (3, True, 37, 4),
+                                       (3, False, 130, 16)])
+def test_tile_layout_e29(orc, m, inc, n, T):
+    """E29: every rank gets one position, positions are distinct, tiles are
+    contiguous slots in launch order, and the holes are exactly the elements
+    cut by n (none when T divides n')."""
+    pos, L = orc.below_tile_layout(m, inc, n, T)
+    V = orc.domain_volume(m, inc, n)
+    assert len(pos) == V and (pos >= 0).all() and len(np.unique(pos)) == V and pos.max() < L
+    nint = n + 2 if (m == 3 and inc) else n
+    if nint % T == 0:
+        assert L == V
+    else:
+        assert L > V
+    # the streaming checksum walks the same layout
+    cs = orc.cs_below_tiles("index_write", m, inc, n, T)
+    M = 1 << 64
+    assert cs["count"] == V
+    assert cs["s1"] == int(sum((int(p) + 1) * r for r, p in enumerate(pos)) % M)
+
+
+@pytest.mark.parametrize("m,n,T", [(2, 1000, 32), (2, 70000, 128), (3, 1100, 32), (3, 300, 8)])
+@pytest.mark.parametrize("diag", ["strict", "inclusive"])
+def test_host_plan_tile_layout_bytes(orc, m, n, T, diag):
+    import paper_1610_07394_b200 as sm
+    if m == 3 and diag == "inclusive":
+        pytest.skip("the m=3 tile-blocked layout is for the strict diagonal")
+    plan = sm.smap_plan(m, n, T, map="below", diag=diag, granularity="tile", layout="tiles", device=sm.DEVICE_NONE)
+    V = orc.domain_volume(m, diag == "inclusive", n)
+    if n <= 1100 and (m == 2 or n <= 300):
+        _, L = orc.below_tile_layout(m, diag == "inclusive", n, T)
+    else:                                   # closed form: full tiles T^m plus the class-sized diagonal slots
+        L = None
+    nb = sm.smap_out_bytes(plan, "index_write")
+    elem = 8 if V > (1 << 32) else 4
+    if L is not None:
+        assert nb == L * elem
+    assert nb >= V * elem
+    with pytest.raises(sm.SmapError):                                        # no O(1) inverse for E29
+        sm.smap_locate(plan, *((2, 1) if m == 2 else (1, 2, 3)))
