@@ -98,12 +98,21 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU oracle legs
+def host_cores():
+    """The host cores this process may run on (torchrun sets OMP_NUM_THREADS=1
+    for its workers; the oracle legs ask for the cores explicitly)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def oracle_sample(rows_lo, rows_hi, nthreads=0):
     """Oracle EDM (fp32 distances + streaming checksum) over rows [lo, hi)."""
     import oracle
     p = workloads.points(N_POINTS, workloads.SEED_C2)
     t0 = time.perf_counter()
-    cs = oracle.cs_edm(p, rows_lo, rows_hi, nthreads=nthreads)
+    cs = oracle.cs_edm(p, rows_lo, rows_hi, nthreads=nthreads or host_cores())
     dt = time.perf_counter() - t0
     return cs, dt
 
@@ -121,8 +130,7 @@ def pick_sample_rows(target_pairs):
 
 
 def cpu_baseline(target_core_seconds=20.0):
-    import oracle
-    cores = oracle.max_threads()
+    cores = host_cores()
     # calibrate on a small sample, then size the sample for ~target_core_seconds of CPU work
     lo, hi, pairs = pick_sample_rows(2e7)
     cs, dt = oracle_sample(lo, hi)
@@ -153,8 +161,7 @@ def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
-    import oracle
-    cores = oracle.max_threads()
+    cores = host_cores()
     lo, hi, pairs = pick_sample_rows(1.5e8)
     for _ in range(args.warmup):
         oracle_sample(lo, hi)
@@ -303,12 +310,19 @@ def main():
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    # test hook for the N > 1 flow on a one-GPU box: every rank on cuda:0 over gloo
+    # (the numbers of such a run are meaningless; the driver's runs never set it)
+    if os.environ.get("SMAP_BENCH_ONE_GPU") == "1":
+        local = 0
     G = world
     assert G == args.gpus or args.gpus == 1 and G == 1, f"--gpus {args.gpus} but WORLD_SIZE={G}"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if G > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("SMAP_BENCH_ONE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
 
     n = N_POINTS
@@ -387,7 +401,7 @@ def main():
         if G > 1:
             r = torch.tensor([st["count"], st["xr"] - (1 << 64) if st["xr"] >= (1 << 63) else st["xr"]],
                              dtype=torch.int64).to(dev)
-            g2 = torch.zeros(G, 2, dtype=torch.int64, device=dev)
+            g2 = torch.zeros(G * 2, dtype=torch.int64, device=dev)
             dist.all_gather_into_tensor(g2, r)
             g2.cpu()
     e1.record(stream)
@@ -446,7 +460,7 @@ def main():
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
         key = json.dumps({k: cfg[k] for k in sorted(cfg)}, sort_keys=True)
-        traffic = tr.get(key)
+        traffic = tr.get(key) if G == 1 else None      # (the capture is of the unsharded launch)
     except (OSError, ValueError):
         pass
     # the stricter denominator for a write-bound kernel: a write-only fill of the
