@@ -58,6 +58,8 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.rows = []
+        self.stamps = []
+        self.t_region = None
         self.proc = None
         self.thread = None
 
@@ -75,11 +77,25 @@ class Clocks:
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
+            self.stamps.append(time.perf_counter())
+
+    def wait_first(self, timeout=3.0):
+        """Block until nvidia-smi has produced its first sample (its start-up
+        takes ~0.1-1 s), so that the samples cover the timed region."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+        self.t_region = time.perf_counter()
 
     def stop(self):
         if self.proc is None:
             return None
+        t_end = time.perf_counter()
         time.sleep(0.15)
+        # keep the samples taken during the timed region (plus one sampling period)
+        if self.t_region is not None:
+            keep = [r for r, t in zip(self.rows, self.stamps) if self.t_region <= t <= t_end + 0.1]
+            self.rows = keep or self.rows[-1:]
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -293,7 +309,7 @@ def config_table(sm, torch, stream, peak_gbs, reps=10):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)     # ~0.24 s timed: a few clock samples
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -365,6 +381,7 @@ def main():
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = Clocks(local)
     clocks.start()
+    clocks.wait_first()
     barrier()
     t0.record(stream)
     for k in range(args.steps):

@@ -72,6 +72,7 @@ def main():
     dev = torch.cuda.get_device_properties(0)
     table = {"device": dev.name, "sms": dev.multi_processor_count, "configs": {}}
     thread2 = ("thread_rho16", dict(rho=16, granularity="thread"))
+    thread2b = ("thread_rho32", dict(rho=32, granularity="thread"))
     if "C1" in only:
         n = 1024
         out = torch.empty(sm.smap_volume(2, n, "inclusive"), dtype=torch.int32, device="cuda")
@@ -84,7 +85,7 @@ def main():
         p = torch.from_numpy(workloads.points(n, workloads.SEED_C2)).cuda()
         out = torch.empty(sm.smap_volume(2, n), dtype=torch.float32, device="cuda")
         T = dict(granularity="tile", layout="tiles")
-        table["configs"]["C2"] = compare(2, n, "edm", [thread2, ("tile_rho256_rows", dict(rho=256, granularity="tile")),
+        table["configs"]["C2"] = compare(2, n, "edm", [thread2, thread2b, ("tile_rho256_rows", dict(rho=256, granularity="tile")),
                                                         ("tile_rho128_tiles", dict(rho=128, **T)),
                                                         ("tile_rho128_tiles_xor", dict(rho=128, flags=sm.RUN_XOR, **T)),
                                                         ("tile_rho128_tiles_p4_xor", dict(rho=128, persistent=4, flags=sm.RUN_XOR, **T)),
@@ -114,7 +115,7 @@ def main():
     if "C4" in only:
         n = 1 << 17
         out = torch.empty(sm.smap_volume(2, n), dtype=torch.int64, device="cuda")
-        table["configs"]["C4"] = compare(2, n, "index_write", [thread2, ("tile_rho128", dict(rho=128, granularity="tile")),
+        table["configs"]["C4"] = compare(2, n, "index_write", [thread2, thread2b, ("tile_rho128", dict(rho=128, granularity="tile")),
                                                                 ("tile_rho256", dict(rho=256, granularity="tile")),
                                                                 ("tile_rho512", dict(rho=512, granularity="tile")),
                                                                 ("tile_rho128_tiles", dict(rho=128, granularity="tile", layout="tiles")),
