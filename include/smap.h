@@ -62,8 +62,8 @@ typedef enum {
                                 S_s = [O_s, O_s + N_s), N_0 > N_1 > ...); every piece is a power-of-two
                                 simplex mapped by lambda (lambda2 inclusive tile grid, lambda3 for
                                 N_s >= 8) or a box / small simplex at the identity, so every launched
-                                tile holds elements (besides lambda3's own idle tiles).  Any n; TILE
-                                granularity, unsharded.  With SMAP_LAYOUT_TILES (reading E29) every
+                                tile holds elements (besides lambda3's own idle tiles).  Any n;
+                                THREAD (blocks, the paper's launch) or TILE granularity, unsharded.  With SMAP_LAYOUT_TILES (reading E29) every
                                 tile is one slot in launch order whose size depends on its class only
                                 (T^m, diagonal/face, body); elements of a tile cut by n leave holes,
                                 so smap_out_bytes may exceed V * sizeof(element); no smap_locate. */

@@ -163,7 +163,6 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     const bool enm = d->map == SMAP_MAP_ENUM;
     const bool below = d->map == SMAP_MAP_BELOW;
     if (enm && tile) return fail(SMAP_E_INVALID, "the enumeration baseline map is THREAD granularity only");
-    if (below && !tile) return fail(SMAP_E_INVALID, "the approach-from-below map is TILE granularity only");
 
     if (d->diag != SMAP_DIAG_STRICT && d->diag != SMAP_DIAG_INCLUSIVE) return fail(SMAP_E_INVALID, "bad diag %d", d->diag);
     if (d->granularity != SMAP_GRAN_THREAD && d->granularity != SMAP_GRAN_TILE)

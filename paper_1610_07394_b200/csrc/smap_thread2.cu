@@ -106,6 +106,9 @@ cudaError_t launch_thread2(const Params &P, int map, bool incl, int pl, int cs, 
 {
     if (map == SMAP_MAP_LAMBDA) return incl ? pick_pl<SMAP_MAP_LAMBDA, true>(P, pl, cs, s) : pick_pl<SMAP_MAP_LAMBDA, false>(P, pl, cs, s);
     if (map == SMAP_MAP_ENUM) return incl ? pick_pl<SMAP_MAP_ENUM, true>(P, pl, cs, s) : pick_pl<SMAP_MAP_ENUM, false>(P, pl, cs, s);
+    // approach n from below (E28): the decode yields off-diagonal blocks and single diagonal
+    // blocks, so the threads filter like BB (j < i / j <= i on the element coordinates)
+    if (map == SMAP_MAP_BELOW) return incl ? pick_pl<SMAP_MAP_BELOW, true>(P, pl, cs, s) : pick_pl<SMAP_MAP_BELOW, false>(P, pl, cs, s);
     return incl ? pick_pl<SMAP_MAP_BB, true>(P, pl, cs, s) : pick_pl<SMAP_MAP_BB, false>(P, pl, cs, s);
 }
 

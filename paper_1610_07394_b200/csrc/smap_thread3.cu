@@ -11,6 +11,8 @@ template <int MAP, int PL, int CS>
 __global__ void __launch_bounds__(512) k_thread3(Params P)
 {
     constexpr bool LAM = MAP == SMAP_MAP_LAMBDA;
+    constexpr bool BEL = MAP == SMAP_MAP_BELOW;   // E28: lambda3 classes (0/1/2/3) plus BB-like faces 5/6
+    constexpr bool LL = LAM || BEL;
     const uint64_t bid = blockIdx.x;
     const uint32_t a = threadIdx.x, bb = threadIdx.y, c = threadIdx.z, rho = (uint32_t)P.rho;
     const Blk3 B = decode3<MAP>(bid, P);
@@ -25,7 +27,7 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
         return;
     }
     // blocks with no element at all exit as a whole (lambda: idle spare/filler; BB: outside)
-    if (PL != PL_TDUMP && ((LAM && B.cls == 3) || (!LAM && B.cls == 4))) {
+    if (PL != PL_TDUMP && ((LL && B.cls == 3) || (!LL && B.cls == 4))) {
         if (pl_atm(PL)) {                 // ATM writes one partial per block
             if (a == 0 && bb == 0 && c == 0) P.partials[bid] = 0.0;
         }
@@ -36,7 +38,7 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
     // element coordinates also as (slot, local) pairs: slot 0/1/2 = block I/J/K
     uint32_t si = 0, li = a, sj = 1, lj = bb, sk = 2, lk = c;
     bool valid;
-    if (!LAM) {
+    if (!LL || (BEL && (B.cls == 5 || B.cls == 6))) {   // identity + filter (BB; below's face blocks)
         i = B.I * rho + a; j = B.J * rho + bb; k = B.K * rho + c;
         valid = (B.cls != 4) && i < j && j < k;
     } else if (B.cls == 3) {
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(512) k_thread3(Params P)
         // useful elements of this block in closed form (no second barrier)
         const uint32_t r3 = rho * rho * rho, face = rho * rho * (rho - 1), body = rho * (rho - 1) * (rho - 2) / 6;
         uint32_t cnt;
-        if (LAM) cnt = B.cls == 2 ? body : (B.I < B.J ? r3 : face);
+        if (LL && B.cls <= 2) cnt = B.cls == 2 ? body : (B.I < B.J ? r3 : face);
         else cnt = B.cls == 0 ? r3 : (B.cls == 2 ? body : face / 2);
         if ((B.K + 1) * rho > (uint32_t)P.n) cnt = __syncthreads_count(valid);   // block cut by n (block-uniform)
         if (pl_atm(PL)) {
@@ -153,6 +155,7 @@ cudaError_t launch_thread3(const Params &P, int map, int pl, int cs, cudaStream_
 {
     if (map == SMAP_MAP_LAMBDA) return pick3<SMAP_MAP_LAMBDA>(P, pl, cs, s);
     if (map == SMAP_MAP_ENUM) return pick3<SMAP_MAP_ENUM>(P, pl, cs, s);
+    if (map == SMAP_MAP_BELOW) return pick3<SMAP_MAP_BELOW>(P, pl, cs, s);
     return pick3<SMAP_MAP_BB>(P, pl, cs, s);
 }
 

@@ -71,6 +71,29 @@ def main():
         rows.append(row)
         del out
         torch.cuda.empty_cache()
+    # the paper's launch (one element per thread, rho^m threads per block): block-launch bound,
+    # so the from-below decomposition's fewer blocks show directly
+    for m, n, payload, rho, seed, param in [(2, 40000, "edm", 16, workloads.SEED_C2, 0.0),
+                                            (2, 70000, "index_write", 16, None, 0.0),
+                                            (3, 1100, "index_write", 8, None, 0.0),
+                                            (3, 1100, "tc", 8, workloads.SEED_C5, 0.5),
+                                            (3, 1500, "atm", 8, workloads.SEED_C3, 1e-2)]:
+        pts = torch.from_numpy(workloads.points(n, seed)).cuda() if seed else None
+        row = {"m": m, "n": n, "payload": payload, "granularity": "thread", "rho": rho, "elements": sm.smap_volume(m, n)}
+        out = None
+        for mp in ("below", "lambda", "bb"):
+            plan = sm.smap_plan(m, n, rho, map=mp, granularity="thread")
+            if out is None:
+                out = sm.alloc_out(plan, payload)
+            ms = med(plan, payload, pts, param, out, 0, max(3, a.reps // 2))
+            q = sm.smap_plan_query(plan)
+            row[mp] = {"ms": round(ms, 4), "blocks": q["grid_blocks"], "launched": q["launched_threads"]}
+        row["above_over_below"] = round(row["lambda"]["ms"] / row["below"]["ms"], 3)
+        row["bb_over_below"] = round(row["bb"]["ms"] / row["below"]["ms"], 3)
+        print(json.dumps(row), flush=True)
+        rows.append(row)
+        del out
+        torch.cuda.empty_cache()
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/below.json", "w") as f:
         json.dump({"device": torch.cuda.get_device_name(0), "rows": rows}, f, indent=1)

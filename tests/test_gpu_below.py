@@ -185,3 +185,38 @@ def test_tile_layout_edm_full_size(sm, orc):
     assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
     del out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("m,n,rho", [(2, 1000, 16), (2, 3001, 32), (2, 100, 8), (3, 300, 8), (3, 45, 4), (3, 129, 8)])
+@pytest.mark.parametrize("diag", ["strict", "inclusive"])
+def test_thread_granularity(sm, orc, m, n, rho, diag):
+    """The paper's launch (rho^m threads per block) over the below
+    decomposition: same block records, exact cover, index write."""
+    plan = sm.smap_plan(m, n, rho, map="below", diag=diag, granularity="thread")
+    nint = n + 2 if (m == 3 and diag == "inclusive") else n
+    out, _ = run(sm, plan, "map_dump")
+    np.testing.assert_array_equal(out.cpu().numpy().reshape(-1, 4), orc.below_tiles(m, -(-nint // rho)))
+    out, _ = run(sm, plan, "hitcount", zero=True)
+    assert bool((out == 1).all())
+    out, st = run(sm, plan, "index_write", flags=sm.RUN_CHECKSUM_MIX)
+    exp = orc.index_write(m, diag == "inclusive", n)
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), exp)
+    cs = orc.cs_array(exp)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+
+
+@pytest.mark.parametrize("n,rho", [(300, 8), (250, 4), (129, 8)])
+def test_thread_granularity_payloads(sm, orc, n, rho):
+    p = workloads.points(n, workloads.SEED_C3)
+    dp = dev(p)
+    plan = sm.smap_plan(3, n, rho, map="below", granularity="thread")
+    V = math.comb(n, 3)
+    ref = orc.atm_sum(p, np.float32(1e-2))
+    _, st = run(sm, plan, "atm", points=dp, param=1e-2)
+    assert st["count"] == V and abs(st["sum"] - ref) <= 1e-5 * abs(ref)
+    _, st = run(sm, plan, "tc", points=dp, param=0.5)
+    assert st["count"] == V and st["tc"] == orc.tc_count(p, np.float32(0.5))
+    p2 = workloads.points(1000, workloads.SEED_C2)
+    plan2 = sm.smap_plan(2, 1000, 16, map="below", granularity="thread")
+    out, _ = run(sm, plan2, "edm", points=dev(p2), flags=sm.RUN_XOR)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), orc.edm(p2).view(np.uint32))

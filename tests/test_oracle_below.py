@@ -124,8 +124,8 @@ def test_host_plan_counts(orc, m, n, T, diag):
 def test_host_plan_rejects(orc):
     import paper_1610_07394_b200 as sm
     N = sm.DEVICE_NONE
-    with pytest.raises(sm.SmapError):
-        sm.smap_plan(2, 1000, 16, map="below", device=N)                      # THREAD granularity
+    with pytest.raises(sm.SmapError):                                        # THREAD + tile layout
+        sm.smap_plan(2, 1000, 16, map="below", layout="tiles", device=N)
     with pytest.raises(sm.SmapError):
         sm.smap_plan(2, 1000, 32, map="below", granularity="tile", shard_count=2, device=N)
     with pytest.raises(sm.SmapError):                                        # m=3 inclusive tile layout
