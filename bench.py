@@ -151,13 +151,18 @@ def cpu_baseline(target_core_seconds=20.0):
     lo, hi, pairs = pick_sample_rows(2e7)
     cs, dt = oracle_sample(lo, hi)
     rate = pairs / max(dt, 1e-6)                                  # pairs per wall second on all cores
-    want = max(2e7, min(rate * target_core_seconds / max(cores, 1), 1.5e9))
+    want = max(2e7, min(rate * target_core_seconds / max(cores, 1), 3e9))
     lo, hi, pairs = pick_sample_rows(want)
     cs, dt = oracle_sample(lo, hi)
+    # the plain single-thread oracle on a smaller sample
+    lo1, hi1, pairs1 = pick_sample_rows(2.5e8)
+    _, dt1 = oracle_sample(lo1, hi1, nthreads=1)
     return {"value": pairs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"rows {lo}..{hi - 1} of the n={N_POINTS} strict EDM ({pairs} pairs: fp32 distances + "
                       f"linear/mix checksums, {cores} OpenMP threads, {dt:.2f} s wall)",
-            "seconds": dt}
+            "seconds": dt,
+            "single_thread": {"value": pairs1 / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"rows {lo1}..{hi1 - 1} ({pairs1} pairs), {dt1:.2f} s wall"}}
 
 
 def bench_config(G):
