@@ -66,7 +66,8 @@ typedef enum {
                                 THREAD (blocks, the paper's launch) or TILE granularity, unsharded.  With SMAP_LAYOUT_TILES (reading E29) every
                                 tile is one slot in launch order whose size depends on its class only
                                 (T^m, diagonal/face, body); elements of a tile cut by n leave holes,
-                                so smap_out_bytes may exceed V * sizeof(element); no smap_locate. */
+                                so smap_out_bytes may exceed V * sizeof(element).  smap_locate
+                                inverts it (piece lookup + closed form, host). */
 } smap_map;
 
 typedef enum {
@@ -243,7 +244,7 @@ smap_status smap_result_combine(const void *records, int count, void *dst, void 
  * SMAP_LAYOUT_TILES: the position in the shard-local tile-blocked array).
  * Host only, O(1) (lambda2^-1 via b = 2^floor(log2(I xor J)), q = I >> (log2 b + 1)).
  * SMAP_E_INVALID for an element outside the domain; SMAP_E_UNSUPPORTED for m=3 with
- * shard_count > 1 and for BELOW plans with the tile-blocked layout. */
+ * shard_count > 1. */
 smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *pos);
 
 /* Useful-element count V of a domain: C(n,2), n(n+1)/2 or C(n,3).  Host only. */

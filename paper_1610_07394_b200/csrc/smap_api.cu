@@ -31,6 +31,7 @@ struct smap_plan_s {
     double *d_scratch = nullptr;
     uint32_t *d_adj = nullptr;      // TC pair-predicate bitmap (TILE)
     Piece *d_pieces = nullptr;      // SMAP_MAP_BELOW decomposition
+    std::vector<uint32_t> segN, segO;   // SMAP_MAP_BELOW: the binary-digit segments of M (sizes, offsets)
     uint64_t layout_len = 0;        // SMAP_MAP_BELOW tile-blocked layout: slots incl. holes (E29)
     std::vector<Piece> pieces;
     float *d_stage = nullptr;
@@ -72,9 +73,9 @@ static int ilog2(int64_t x) { int l = 0; while ((int64_t)1 << (l + 1) <= x) l++;
 
 // "Approach n from below" (reading E28): the pieces of the M-tile
 // simplex in launch order (include/smap.h); returns the total tile count.
-static uint64_t below_pieces(int m, int64_t M, int T, bool incl, std::vector<Piece> &out, uint64_t *slots)
+static uint64_t below_pieces(int m, int64_t M, int T, bool incl, std::vector<Piece> &out, uint64_t *slots,
+                             std::vector<uint32_t> &Ns, std::vector<uint32_t> &Os)
 {
-    std::vector<uint32_t> Ns, Os;
     for (int64_t rest = M, off = 0; rest > 0;) {        // binary digits of M, largest first
         const int64_t b = (int64_t)1 << ilog2(rest);
         Ns.push_back((uint32_t)b); Os.push_back((uint32_t)off);
@@ -216,7 +217,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
         const int64_t M = (nint + rho - 1) / rho;
         P.N = (int)M; P.log2N = 0;
         P.W = (int)M; P.log2W = 0; P.wx0 = 0;
-        P.nblocks = below_pieces(m, M, rho, incl, p->pieces, &p->layout_len);
+        P.nblocks = below_pieces(m, M, rho, incl, p->pieces, &p->layout_len, p->segN, p->segO);
         P.npieces = (int)p->pieces.size();
     } else if (lam) {
         P.W = (int)(N / 2 / G); P.log2W = ilog2(P.W); P.wx0 = d->shard_rank * P.W;
@@ -442,12 +443,128 @@ smap_status smap_stats_fetch(smap_plan_t p, smap_stats *st)
 
 static int floor_log2_u64(uint64_t y) { return 63 - __builtin_clzll(y); }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------- E29 inverse
+// Grid id of the tile (J, I), J <= I, in the lambda2 inclusive tile grid of side
+// N = 2^e (row order; rows 0 and N hold the diagonal tiles): lambda2^-1 as in E23.
+static uint64_t tri_grid_id(uint64_t J, uint64_t I, int e)
+{
+    if (e == 0) return 0;
+    const uint64_t N = 1ull << e, W = N / 2;
+    if (I == J) return I < W ? I : N * W + (I - W);
+    const int l = 63 - __builtin_clzll(I ^ J);
+    const uint64_t b = 1ull << l, q = I >> (l + 1);
+    return (I - 2 * q * b) * W + (J - q * b);
+}
+static uint64_t tri_slot_h(uint64_t g, int e, uint64_t sd, uint64_t sf)      // = below_tri_slot
+{
+    if (e == 0) return 0;
+    const uint64_t W = 1ull << (e - 1), N = W << 1;
+    if (g < W) return g * sd;
+    if (g < N * W) return W * sd + (g - W) * sf;
+    return W * sd + (N - 1) * W * sf + (g - N * W) * sd;
+}
+
+// Position of element e in the E29 layout of a below plan: the segments of
+// the element's tiles give the piece, the piece's closed form the slot, the
+// segment kind the place inside the slot.  O(#pieces) piece lookup (host).
+static smap_status locate_below(smap_plan_t p, const int64_t *e, int *shard, uint64_t *pos)
+{
+    const smap_plan_desc &d = p->d;
+    const bool incl = d.diag == SMAP_DIAG_INCLUSIVE;
+    const int64_t n = d.n;
+    const uint64_t T = (uint64_t)d.rho;
+    auto seg = [&](uint64_t X) {
+        int s = 0;
+        while (s + 1 < (int)p->segO.size() && X >= p->segO[s + 1]) s++;
+        return s;
+    };
+    auto piece = [&](int kind, int a, int b, int c) -> const Piece * {
+        for (const Piece &pc : p->pieces)
+            if (pc.kind == kind && pc.Oa == p->segO[a] && pc.Ob == p->segO[b] && pc.Oc == p->segO[c]) return &pc;
+        return nullptr;
+    };
+    *shard = 0;
+    if (d.m == 2) {
+        const int64_t i = e[0], j = e[1];
+        if (!(0 <= j && j < n && i < n && (incl ? j <= i : j < i))) return fail(SMAP_E_INVALID, "element outside the domain");
+        const uint64_t I = (uint64_t)i / T, J = (uint64_t)j / T, r = (uint64_t)i % T, c = (uint64_t)j % T;
+        const int a = seg(J), b = seg(I);
+        const Piece *pc = piece(a == b ? PK_TRI2 : PK_RECT2, a, b, b);
+        if (!pc && a == b) pc = piece(PK_TRI2, a, a, a);
+        if (!pc) return fail(SMAP_E_CUDA, "smap_locate: piece not found (internal)");
+        const uint64_t sd = incl ? T * (T + 1) / 2 : T * (T - 1) / 2;
+        uint64_t slot;
+        if (a == b) slot = pc->sbase + tri_slot_h(tri_grid_id(J - pc->Oa, I - pc->Oa, pc->ea), pc->ea, sd, T * T);
+        else slot = pc->sbase + ((I - pc->Ob) * (1ull << pc->ea) + (J - pc->Oa)) * T * T;
+        const uint64_t in = I != J ? r * T + c : incl ? r * (r + 1) / 2 + c : r * (r - 1) / 2 + c;
+        *pos = slot + in;
+        return SMAP_OK;
+    }
+    const int64_t i = e[0], j = e[1], k = e[2];
+    if (!(0 <= i && i < j && j < k && k < n)) return fail(SMAP_E_INVALID, "element outside the domain");
+    const uint64_t bi = (uint64_t)i / T, bj = (uint64_t)j / T, bk = (uint64_t)k / T;
+    const uint64_t il = (uint64_t)i % T, jl = (uint64_t)j % T, kl = (uint64_t)k % T;
+    const int a = seg(bi), b = seg(bj), c = seg(bk);
+    const uint64_t T3 = T * T * T, Tf = T * T * (T - 1) / 2;
+    const int kind = (bi == bj && bj == bk) ? 3 : bi == bj ? 1 : bj == bk ? 2 : 0;
+    uint64_t slot, half = 0;
+    if (a == c) {
+        const uint64_t O = p->segO[a], N = p->segN[a];
+        const Piece *pc = piece(N >= 8 ? PK_TET3 : PK_TETS, a, a, a);
+        if (!pc) return fail(SMAP_E_CUDA, "smap_locate: piece not found (internal)");
+        const uint64_t I = bi - O, J = bj - O, K = bk - O;
+        if (N < 8) {
+            slot = pc->sbase + tile_slot3_bb(I, J, K, T);
+        } else {                                 // lambda3^-1 inside the piece (as for the lambda layout)
+            const uint64_t h = N / 2;
+            uint64_t wx, wy, wz;
+            if (kind == 3) {
+                if (I < h) { wx = I; wy = 0; wz = h; } else { wx = I - h; wy = 0; wz = h + 1; }
+            } else {
+                const uint64_t Z = kind == 0 ? J - I : 0;
+                if (kind == 2) half = Tf;
+                const int l = 63 - __builtin_clzll(I ^ K);
+                const uint64_t bb = 1ull << l, q = I >> (l + 1);
+                const uint64_t u0 = I - 2 * q * bb, v0 = K - 2 * q * bb - bb;
+                uint64_t u, v, w;
+                if (Z < bb) { u = u0; v = v0; w = Z; }
+                else { u = bb - 1 - u0; v = bb - 1 - v0; w = 2 * bb - 1 - Z; }
+                if (bb == h) { wx = u; wy = v; wz = w; }
+                else { wx = q * bb + u; wy = bb + v; wz = h + w; }
+            }
+            slot = pc->sbase + tile_slot3_lambda(wx, wy, wz, h, h, T);
+        }
+    } else if (b == c) {                         // I in S_a x triangle J <= K of S_b
+        const Piece *pc = piece(PK_LT, a, b, c);
+        if (!pc) return fail(SMAP_E_CUDA, "smap_locate: piece not found (internal)");
+        const uint64_t h = tri_grid_id(bj - pc->Ob, bk - pc->Ob, pc->eb), x = bi - pc->Oa;
+        slot = pc->sbase + (1ull << pc->ea) * tri_slot_h(h, pc->eb, Tf, T3) + x * (bj == bk ? Tf : T3);
+    } else if (a == b) {                         // triangle I <= J of S_a x K in S_c
+        const Piece *pc = piece(PK_TL, a, b, c);
+        if (!pc) return fail(SMAP_E_CUDA, "smap_locate: piece not found (internal)");
+        const uint64_t Na = 1ull << pc->ea;
+        const uint64_t total = pc->ea == 0 ? Tf : Na * Tf + (Na / 2) * (Na - 1) * T3;
+        const uint64_t h = tri_grid_id(bi - pc->Oa, bj - pc->Oa, pc->ea);
+        slot = pc->sbase + (bk - pc->Oc) * total + tri_slot_h(h, pc->ea, Tf, T3);
+    } else {
+        const Piece *pc = piece(PK_BOX, a, b, c);
+        if (!pc) return fail(SMAP_E_CUDA, "smap_locate: piece not found (internal)");
+        const uint64_t g = (bi - pc->Oa) + (1ull << pc->ea) * ((bj - pc->Ob) + (1ull << pc->eb) * (bk - pc->Oc));
+        slot = pc->sbase + g * T3;
+    }
+    *pos = slot + half + seg3_local(kind, il, jl, kl, T);
+    return SMAP_OK;
+}
+
+extern "C" {
+
 smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *pos)
 {
     if (!p || !e || !shard || !pos) return fail(SMAP_E_INVALID, "smap_locate: NULL argument");
     const smap_plan_desc &d = p->d;
-    if (d.map == SMAP_MAP_BELOW && d.layout == SMAP_LAYOUT_TILES)
-        return fail(SMAP_E_UNSUPPORTED, "smap_locate: no O(1) inverse for the approach-from-below tile layout");
+    if (d.map == SMAP_MAP_BELOW && d.layout == SMAP_LAYOUT_TILES) return locate_below(p, e, shard, pos);
     const bool lam = d.map == SMAP_MAP_LAMBDA, incl = d.diag == SMAP_DIAG_INCLUSIVE;
     const int64_t n = d.n;
     if (d.m == 3) {

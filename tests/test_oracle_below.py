@@ -171,5 +171,31 @@ def test_host_plan_tile_layout_bytes(orc, m, n, T, diag):
     if L is not None:
         assert nb == L * elem
     assert nb >= V * elem
-    with pytest.raises(sm.SmapError):                                        # no O(1) inverse for E29
-        sm.smap_locate(plan, *((2, 1) if m == 2 else (1, 2, 3)))
+    if L is not None and V <= 600000:                  # smap_locate inverts E29 (host): every element
+        pos, _ = orc.below_tile_layout(m, diag == "inclusive", n, T)
+        got = _locate_all(sm, plan, m, n, diag == "inclusive")
+        np.testing.assert_array_equal(got, pos)
+
+
+def _locate_all(sm, plan, m, n, inc):
+    out = []
+    if m == 2:
+        for i in range(n):
+            for j in range(i + 1 if inc else i):
+                out.append(sm.smap_locate(plan, i, j)[1])
+    else:
+        for k in range(n):
+            for j in range(k):
+                for i in range(j):
+                    out.append(sm.smap_locate(plan, i, j, k)[1])
+    return np.array(out, np.int64)
+
+
+@pytest.mark.parametrize("m,inc,n,T", [(2, False, 333, 32), (2, True, 700, 64), (2, False, 130, 32), (2, True, 1000, 32),
+                                       (3, False, 100, 8), (3, False, 130, 16), (3, False, 64, 8), (3, False, 99, 8)])
+def test_locate_inverts_e29(orc, m, inc, n, T):
+    import paper_1610_07394_b200 as sm
+    plan = sm.smap_plan(m, n, T, map="below", diag="inclusive" if inc else "strict", granularity="tile",
+                        layout="tiles", device=sm.DEVICE_NONE)
+    pos, _ = orc.below_tile_layout(m, inc, n, T)
+    np.testing.assert_array_equal(_locate_all(sm, plan, m, n, inc), pos)
