@@ -87,3 +87,20 @@ def test_extreme_sizes_host_plans(sm):
     for m, n_, d in ((2, 2, "strict"), (3, 3, "strict"), (3, 1, "inclusive"), (2, 1, "inclusive")):
         q = sm.smap_plan_query(sm.smap_plan(m, n_, 1, map="bb", diag=d, device=N))
         assert q["useful_elems"] == sm.smap_volume(m, n_, d)
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    exe = str(tmp_path / "edm_c_api")
+    pkg = os.path.join(ROOT, "paper_1610_07394_b200")
+    cmd = ["gcc", "-O2", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "examples", "edm_c_api.c"), "-L", pkg, "-lsmap", "-L", "/usr/local/cuda/lib64",
+           "-lcudart", "-lm", f"-Wl,-rpath,{pkg}", "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return exe
+
+
+def test_c_example_compiles_against_the_header(tmp_path):
+    """The boundary is a plain C ABI: examples/edm_c_api.c (C, no Python)
+    compiles and links against include/smap.h and libsmap.so."""
+    assert os.path.exists(_build_c_example(tmp_path))

@@ -362,3 +362,13 @@ def test_result_combine_kernel(sm, G):
     assert float(got[6:7].numpy().view(np.float64)[0]) == s
     sm.smap_result_combine(d, G, d[0])                  # dst may alias records[0]
     assert torch.equal(d[0].cpu()[:6], exp[:6])
+
+
+def test_c_example_runs(tmp_path):
+    """examples/edm_c_api.c run as a C program on the GPU: exit 0 means the
+    count and one located distance matched its own fp32 recomputation."""
+    import subprocess
+    import test_abi
+    exe = test_abi._build_c_example(tmp_path)
+    r = subprocess.run([exe, "3000"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
