@@ -131,7 +131,8 @@ typedef struct {
     int     device;       /* CUDA device ordinal; -1 = the calling thread's current device;
                              SMAP_DEVICE_NONE = host-only plan (validation + closed forms; cannot run) */
     int     order;        /* lambda2 launch order (smap_order); ignored otherwise */
-    int     layout;       /* m=2 output layout (smap_layout); TILE granularity only for SMAP_LAYOUT_TILES */
+    int     layout;       /* output layout (smap_layout); SMAP_LAYOUT_TILES needs TILE granularity (m=3
+                             inclusive: BELOW plans only) */
 } smap_plan_desc;
 
 typedef enum {

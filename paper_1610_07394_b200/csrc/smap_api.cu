@@ -200,7 +200,7 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     if (d->layout != SMAP_LAYOUT_ROWS && d->layout != SMAP_LAYOUT_TILES) return fail(SMAP_E_INVALID, "bad layout %d", d->layout);
     if (d->layout == SMAP_LAYOUT_TILES && !tile)
         return fail(SMAP_E_INVALID, "the tile-blocked layout is for TILE plans");
-    if (d->layout == SMAP_LAYOUT_TILES && m == 3 && incl)
+    if (d->layout == SMAP_LAYOUT_TILES && m == 3 && incl && !below)
         return fail(SMAP_E_UNSUPPORTED, "the m=3 tile-blocked layout is for the strict diagonal");
     if (padded && G != 1) return fail(SMAP_E_UNSUPPORTED, "sharding needs n to be a power of two (padded grids are not volume-balanced)");
     if (padded && !below && d->layout == SMAP_LAYOUT_TILES)
@@ -502,8 +502,10 @@ static smap_status locate_below(smap_plan_t p, const int64_t *e, int *shard, uin
         *pos = slot + in;
         return SMAP_OK;
     }
-    const int64_t i = e[0], j = e[1], k = e[2];
-    if (!(0 <= i && i < j && j < k && k < n)) return fail(SMAP_E_INVALID, "element outside the domain");
+    int64_t i = e[0], j = e[1], k = e[2];
+    if (incl ? !(0 <= i && i <= j && j <= k && k < n) : !(0 <= i && i < j && j < k && k < n))
+        return fail(SMAP_E_INVALID, "element outside the domain");
+    if (incl) { j += 1; k += 2; }                       // E24: the strict set of n + 2
     const uint64_t bi = (uint64_t)i / T, bj = (uint64_t)j / T, bk = (uint64_t)k / T;
     const uint64_t il = (uint64_t)i % T, jl = (uint64_t)j % T, kl = (uint64_t)k % T;
     const int a = seg(bi), b = seg(bj), c = seg(bk);

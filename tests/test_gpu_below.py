@@ -128,8 +128,6 @@ SENT = 0x7FABCDEF
 def test_tile_layout_index_write(sm, orc, m, n, T, diag):
     """E29: every packed rank lands at the oracle's position and the holes of
     tiles cut by n are never written."""
-    if m == 3 and diag == "inclusive":
-        pytest.skip("the m=3 tile-blocked layout is for the strict diagonal")
     plan = sm.smap_plan(m, n, T, map="below", diag=diag, granularity="tile", layout="tiles")
     pos, L = orc.below_tile_layout(m, diag == "inclusive", n, T)
     out = sm.alloc_out(plan, "index_write")

@@ -128,8 +128,8 @@ def test_host_plan_rejects(orc):
         sm.smap_plan(2, 1000, 16, map="below", layout="tiles", device=N)
     with pytest.raises(sm.SmapError):
         sm.smap_plan(2, 1000, 32, map="below", granularity="tile", shard_count=2, device=N)
-    with pytest.raises(sm.SmapError):                                        # m=3 inclusive tile layout
-        sm.smap_plan(3, 1000, 32, map="below", diag="inclusive", granularity="tile", layout="tiles", device=N)
+    with pytest.raises(sm.SmapError):                                        # lambda m=3 inclusive tile layout
+        sm.smap_plan(3, 1022, 32, map="lambda", diag="inclusive", granularity="tile", layout="tiles", device=N)
 
 
 @pytest.mark.parametrize("m,inc,n,T", [(2, False, 100, 8), (2, True, 37, 4), (2, False, 64, 8), (2, False, 1000, 32),
@@ -158,8 +158,6 @@ def test_tile_layout_e29(orc, m, inc, n, T):
 @pytest.mark.parametrize("diag", ["strict", "inclusive"])
 def test_host_plan_tile_layout_bytes(orc, m, n, T, diag):
     import paper_1610_07394_b200 as sm
-    if m == 3 and diag == "inclusive":
-        pytest.skip("the m=3 tile-blocked layout is for the strict diagonal")
     plan = sm.smap_plan(m, n, T, map="below", diag=diag, granularity="tile", layout="tiles", device=sm.DEVICE_NONE)
     V = orc.domain_volume(m, diag == "inclusive", n)
     if n <= 1100 and (m == 2 or n <= 300):
@@ -183,16 +181,17 @@ def _locate_all(sm, plan, m, n, inc):
         for i in range(n):
             for j in range(i + 1 if inc else i):
                 out.append(sm.smap_locate(plan, i, j)[1])
-    else:
+    else:                                   # nested-loop (packed rank) order
         for k in range(n):
-            for j in range(k):
-                for i in range(j):
+            for j in range(k + 1 if inc else k):
+                for i in range(j + 1 if inc else j):
                     out.append(sm.smap_locate(plan, i, j, k)[1])
     return np.array(out, np.int64)
 
 
 @pytest.mark.parametrize("m,inc,n,T", [(2, False, 333, 32), (2, True, 700, 64), (2, False, 130, 32), (2, True, 1000, 32),
-                                       (3, False, 100, 8), (3, False, 130, 16), (3, False, 64, 8), (3, False, 99, 8)])
+                                       (3, False, 100, 8), (3, False, 130, 16), (3, False, 64, 8), (3, False, 99, 8),
+                                       (3, True, 100, 8), (3, True, 62, 8)])
 def test_locate_inverts_e29(orc, m, inc, n, T):
     import paper_1610_07394_b200 as sm
     plan = sm.smap_plan(m, n, T, map="below", diag="inclusive" if inc else "strict", granularity="tile",
