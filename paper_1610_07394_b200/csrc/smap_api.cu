@@ -389,11 +389,11 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     P.partials = p->d_partials;
     P.adj = p->d_adj;
     uint32_t launches = 0;
-    CK(cudaMemsetAsync(p->d_res, 0, sizeof(Result), s));
+    if (!tc_bits) CK(cudaMemsetAsync(p->d_res, 0, sizeof(Result), s));   // (the TC pre-pass zeroes it itself)
     CK(cudaEventRecord(p->ev0, s));
     cudaError_t e;
     if (tc_bits) {
-        cudaError_t ea = launch_tc_adjacency(points, (int)d.n, (int)npad, param, p->d_adj, s);
+        cudaError_t ea = launch_tc_adjacency(points, (int)d.n, (int)npad, param, p->d_adj, p->d_res, s);
         if (ea != cudaSuccess) return cuda_fail(ea, "TC adjacency launch");
         launches++;
     }

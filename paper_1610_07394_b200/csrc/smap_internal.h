@@ -143,7 +143,8 @@ cudaError_t launch_tile3(const Params &P, int T, int map, int pl, int cs, unsign
 // TC pre-pass: adj[j * ceil(npad/32) + w] bit b <=> 32w + b < n, j < n and
 // r2(32w + b, j) < R*R (the same fp32 predicate as the per-triple compare);
 // npad = N * rho (rows j < npad, words rounded up).
-cudaError_t launch_tc_adjacency(const float *pts, int n, int npad, float R, uint32_t *adj, cudaStream_t s);
+// It also zeroes the run's result block (the main kernel follows in stream order).
+cudaError_t launch_tc_adjacency(const float *pts, int n, int npad, float R, uint32_t *adj, Result *res, cudaStream_t s);
 // Deterministic fixed-order fp64 reduction of partials[0..np) into res->sum.
 // Adds the number of kernels it launched to *launches.
 cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res,
