@@ -20,7 +20,7 @@ def main():
     runs = 0
     for mp in ("lambda", "bb", "below", "enum"):
         for gran, rho2, rho3 in (("thread", 16, 8), ("tile", 64, 16), ("tile", 128, 32)):
-            if (mp == "below" and gran == "thread") or (mp == "enum" and gran == "tile"):
+            if mp == "enum" and gran == "tile":
                 continue
             for m, n, rho, pts in ((2, 1000, rho2, p2), (3, 300, rho3, p3)):
                 for diag in ("strict", "inclusive"):
@@ -34,6 +34,15 @@ def main():
                                     flags=sm.RUN_CHECKSUM_MIX if pl in ("index_write", "edm", "index_write_atm") else 0)
                         sm.smap_stats_fetch(plan)
                         runs += 1
+    # the E29 tile layout of below plans (any n, holes), incl. the fused payload
+    for m, n, rho, pl in ((2, 1000, 64, "edm"), (2, 1000, 128, "index_write"), (3, 300, 32, "index_write_atm"),
+                          (3, 300, 16, "index_write")):
+        pts = torch.from_numpy(workloads.points(n, 4)).cuda()
+        plan = sm.smap_plan(m, n, rho, map="below", granularity="tile", layout="tiles")
+        out = sm.alloc_out(plan, pl)
+        sm.smap_run(plan, pl, points=pts, param=1e-2, out=out, flags=sm.RUN_CHECKSUM_MIX)
+        sm.smap_stats_fetch(plan)
+        runs += 1
     # tile layouts, sharded
     for m, n, rho in ((2, 1024, 64), (3, 256, 16), (3, 256, 32)):
         pts = torch.from_numpy(workloads.points(n, 3)).cuda()
