@@ -104,3 +104,24 @@ def test_c_example_compiles_against_the_header(tmp_path):
     """The boundary is a plain C ABI: examples/edm_c_api.c (C, no Python)
     compiles and links against include/smap.h and libsmap.so."""
     assert os.path.exists(_build_c_example(tmp_path))
+
+
+def test_result_combine_and_locate_reject_bad_arguments(sm):
+    """Argument checks of smap_result_combine / smap_locate / smap_run happen
+    before any device work (so they run here, without a GPU)."""
+    import ctypes as C
+    lib = sm._lib
+    buf = (C.c_int64 * 16)()
+    assert lib.smap_result_combine(None, 1, C.cast(buf, C.c_void_p), None) == sm.E_INVALID
+    assert lib.smap_result_combine(C.cast(buf, C.c_void_p), 0, C.cast(buf, C.c_void_p), None) == sm.E_INVALID
+    misaligned = C.c_void_p(C.addressof(buf) + 4)
+    assert lib.smap_result_combine(misaligned, 1, C.cast(buf, C.c_void_p), None) == sm.E_INVALID
+    assert "aligned" in sm.smap_last_error()
+    plan = sm.smap_plan(2, 1000, 32, map="below", granularity="tile", layout="tiles", device=sm.DEVICE_NONE)
+    with pytest.raises(sm.SmapError):
+        sm.smap_locate(plan, 5, 7)                       # j > i: outside the strict domain
+    with pytest.raises(sm.SmapError):
+        sm.smap_run(plan, "edm")                         # host-only plan cannot run
+    plan3 = sm.smap_plan(3, 300, 8, map="below", granularity="tile", device=sm.DEVICE_NONE)
+    with pytest.raises(sm.SmapError):
+        sm.smap_locate(plan3, 3, 2, 1)                   # not i < j < k
