@@ -157,3 +157,52 @@ def test_c4_sharded_tiles_partition(sm, orc, G):
         assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
         tot = [(a + b) % (1 << 64) for a, b in zip(tot, (st["count"], st["s0"], st["s1"], st["mix"]))]
     assert tot[0] == V and tot[1] == (V * (V - 1) // 2) % (1 << 64)
+
+
+def test_m3_uint64_index_write_full(sm, orc):
+    """m=3 with V > 2^32 (n = 3000: 4.5e9 triples, 36 GB of uint64 ranks) through
+    the from-below map's E29 tile layout: the u64 tile kernels at full size,
+    streaming checksums against the oracle's walk of the same layout."""
+    n = 3000
+    plan = sm.smap_plan(3, n, 32, map="below", granularity="tile", layout="tiles")
+    out = sm.alloc_out(plan, "index_write")
+    assert out.dtype == torch.int64
+    sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM_MIX)
+    st = sm.smap_stats_fetch(plan)
+    cs = orc.cs_below_tiles("index_write", 3, False, n, 32)
+    assert st["count"] == math.comb(n, 3) == cs["count"]
+    assert (st["s0"], st["s1"], st["mix"]) == (cs["s0"], cs["s1"], cs["mix"])
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_m3_index_write_n2048_tiles_full(sm, orc):
+    """C5's size (n = 2048, 1.43e9 triples) as an index write in the lambda3
+    tile layout (E26) at the bench tile 32: full streaming checksums."""
+    n = 2048
+    plan = sm.smap_plan(3, n, 32, granularity="tile", layout="tiles")
+    out = sm.alloc_out(plan, "index_write")
+    sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM_MIX)
+    st = sm.smap_stats_fetch(plan)
+    cs = orc.cs_tiles3(n, 32)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_m3_uint64_fused_full(sm, orc):
+    """The fused index write + ATM with uint64 ranks (V > 2^32 at n = 3000):
+    index checksums and the fp64 ATM sum against the oracle."""
+    n = 3000
+    p = workloads.points(n, workloads.SEED_C3)
+    plan = sm.smap_plan(3, n, 32, map="below", granularity="tile", layout="tiles")
+    out = sm.alloc_out(plan, "index_write_atm")
+    sm.smap_run(plan, "index_write_atm", points=torch.from_numpy(p).cuda(), param=1e-2, out=out,
+                flags=sm.RUN_CHECKSUM_MIX)
+    st = sm.smap_stats_fetch(plan)
+    del out
+    torch.cuda.empty_cache()
+    cs = orc.cs_below_tiles("index_write", 3, False, n, 32)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
+    ref = orc.atm_sum(p, np.float32(1e-2))
+    assert abs(st["sum"] - ref) <= 1e-5 * abs(ref), (st["sum"], ref)
