@@ -206,3 +206,20 @@ def test_m3_uint64_fused_full(sm, orc):
     assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
     ref = orc.atm_sum(p, np.float32(1e-2))
     assert abs(st["sum"] - ref) <= 1e-5 * abs(ref), (st["sum"], ref)
+
+
+@pytest.mark.parametrize("m,n,rho,mp", [(3, 3000, 8, "lambda"), (3, 3000, 8, "below"), (2, 1 << 17, 16, "lambda"),
+                                        (2, 100000, 16, "below")])
+def test_uint64_index_write_thread_full(sm, orc, m, n, rho, mp):
+    """uint64 ranks at the paper's launch (one element per thread): canonical
+    layout, full streaming checksums (m=3 n=3000: 4.5e9 triples; m=2 n=2^17:
+    8.6e9 pairs = C4)."""
+    plan = sm.smap_plan(m, n, rho, map=mp, granularity="thread")
+    out = sm.alloc_out(plan, "index_write")
+    assert out.dtype == torch.int64
+    sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_CHECKSUM_MIX)
+    st = sm.smap_stats_fetch(plan)
+    del out
+    torch.cuda.empty_cache()
+    cs = orc.cs_index(m, False, n)
+    assert (st["count"], st["s0"], st["s1"], st["mix"]) == (cs["count"], cs["s0"], cs["s1"], cs["mix"])
