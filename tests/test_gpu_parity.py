@@ -372,3 +372,23 @@ def test_c_example_runs(tmp_path):
     exe = test_abi._build_c_example(tmp_path)
     r = subprocess.run([exe, "3000"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("gran,rho", [("thread", 8), ("tile", 16), ("tile", 32)])
+@pytest.mark.parametrize("map_", ["lambda", "below"])
+def test_atm_tc_degenerate_points(sm, orc, gran, rho, map_):
+    """Degenerate point sets: exact duplicates (r^2 = 0, softened by eps^2 for
+    ATM; always inside R for TC) and a tiny-scale cloud (r^2 near the fp32
+    denormal range) -- the packed ATM path falls back to the IEEE-ordered term
+    where its partial is not finite; TC compares the same fp32 r^2."""
+    n = 256
+    for p in (workloads.clustered_points(n, 21), (workloads.points(n, 22) * np.float32(1e-12)).astype(np.float32)):
+        dp = dev_points(p)
+        plan = sm.smap_plan(3, n, rho, map=map_, granularity=gran)
+        _, st = run(sm, plan, "atm", points=dp, param=1e-2)
+        ref = orc.atm_sum(p, np.float32(1e-2))
+        assert st["count"] == math.comb(n, 3)
+        assert abs(st["sum"] - ref) <= 1e-5 * abs(ref), (st["sum"], ref)
+        for R in (0.5, 1e-12, 0.0):
+            _, st = run(sm, plan, "tc", points=dp, param=R)
+            assert st["tc"] == orc.tc_count(p, np.float32(R)), R
