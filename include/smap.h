@@ -95,7 +95,10 @@ typedef enum {
     SMAP_PAYLOAD_INDEX_WRITE = 0, /* out[p] = p; uint32 if V <= 2^32 else uint64 */
     SMAP_PAYLOAD_EDM = 1,         /* m=2 strict: out[p] = ||x_i - x_j||_2, fp32 (E15, E17) */
     SMAP_PAYLOAD_ATM = 2,         /* m=3: sum of Axilrod-Teller terms (E15), param = eps^2; result stats.sum */
-    SMAP_PAYLOAD_TC = 3,          /* m=3: #{i<j<k: r_ij, r_jk, r_ik < R}, param = R; result stats.tc */
+    SMAP_PAYLOAD_TC = 3,          /* m=3: #{i<j<k: r_ij, r_jk, r_ik < R}, param = R; result stats.tc.  TILE plans
+                                     allocate an n'^2 / 8-byte pair-predicate bitmap in the plan's scratch on
+                                     the first TC run (n' = the grid's index range; SMAP_E_NOMEM if it does
+                                     not fit) */
     SMAP_PAYLOAD_MAP_DUMP = 4,    /* int32[4] per grid block/tile in launch order (see below) */
     SMAP_PAYLOAD_HITCOUNT = 5,    /* uint32 out[p] += 1 per mapped element (caller zeroes out) */
     SMAP_PAYLOAD_THREAD_DUMP = 6, /* THREAD gran. only: uint64 per launched thread, p or UINT64_MAX */
