@@ -27,6 +27,10 @@ python scripts/configs_bench.py > $O/${R}_configs.log 2>&1
 cp $O/configs.json $O/${R}_configs.json 2>/dev/null
 python scripts/below_bench.py > $O/${R}_below.log 2>&1
 cp $O/below.json $O/${R}_below_vs_above.json 2>/dev/null
+python scripts/shard_emulation.py > $O/${R}_shards.log 2>&1
+cp $O/shards.json $O/${R}_shard_emulation.json 2>/dev/null
+python scripts/sustained.py > $O/${R}_sustained.log 2>&1
+cp $O/sustained.json $O/${R}_sustained_power_cap.json 2>/dev/null
 # summaries here (ncu is on the box); the large reports stay behind (gpurun_out <= 64 MiB)
 for k in edm_c2 iwa_c3 atm_c3 tc_c5 iw_c4; do
     python scripts/ncu_summary.py $O/${R}_$k.ncu-rep $O/${R}_${k}_ncu_full.json > /dev/null 2>&1
