@@ -4,7 +4,6 @@
 // deterministic fp64 finalize (a7).  No CPU fallback: every payload runs in
 // the sm_100a kernels of smap_thread{2,3}.cu / smap_tile{2,3}.cu.
 #include <cstdio>
-#include <cstdlib>
 #include <cstdarg>
 #include <cstring>
 #include <string>
