@@ -1,9 +1,16 @@
 """Sustained vs burst behaviour under the board power cap: K back-to-back
-launches of the C2 EDM kernel, then K back-to-back write fills of the same
-buffer, per-launch CUDA-event times with nvidia-smi clocks / power sampled
-alongside.  Writes gpurun_out/sustained.json.
+launches of each selected kernel on the C2 output buffer (8.59 GB), with
+per-launch CUDA-event times and nvidia-smi clocks / power sampled alongside.
 
-    python scripts/sustained.py [--k 400]
+  edm   the C2 EDM kernel (bench launch, count + xor reduction)
+  iw    the m=2 u32 index write with the same launch and the same 8.59 GB
+        (SM stores with almost no arithmetic: separates store-path power
+        from EDM arithmetic power)
+  fill  torch's write fill of the same buffer (the write roofline)
+
+Writes gpurun_out/sustained[_TAG].json and prints one summary line per kernel.
+
+    python scripts/sustained.py [--k 400] [--what edm,iw,fill] [--tag base]
 """
 import argparse
 import json
@@ -43,36 +50,47 @@ def run(fn, k):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--k", type=int, default=400)
+    ap.add_argument("--what", default="edm,fill")
+    ap.add_argument("--tag", default="")
+    ap.add_argument("--cool", type=float, default=2.0, help="idle seconds before each kernel's run")
     a = ap.parse_args()
     n = 65536
     pts = torch.from_numpy(workloads.points(n, workloads.SEED_C2)).cuda()
     plan = sm.smap_plan(2, n, **workloads.BENCH_EDM)
     out = sm.alloc_out(plan, "edm")
+    outi = out.view(torch.int32)
     rows, stop = [], threading.Event()
     th = threading.Thread(target=sampler, args=(rows, stop), daemon=True)
     th.start()
     time.sleep(1.0)
+    fns = {"edm": lambda: sm.smap_run(plan, "edm", points=pts, out=out, flags=sm.RUN_XOR),
+           "iw": lambda: sm.smap_run(plan, "index_write", out=outi, flags=sm.RUN_XOR),
+           "fill": lambda: out.zero_()}
     res = {}
-    for name, fn in (("edm", lambda: sm.smap_run(plan, "edm", points=pts, out=out, flags=sm.RUN_XOR)),
-                     ("fill", lambda: out.zero_())):
-        time.sleep(1.0)                                   # let the board cool down between the two
+    for name in a.what.split(","):
+        time.sleep(a.cool)                                 # let the board cool down between kernels
         t0 = time.perf_counter()
-        ts = run(fn, a.k)
+        ts = run(fns[name], a.k)
         t1 = time.perf_counter()
         smp = [r for t, r in rows if t0 <= t <= t1]
+        tail = [r for t, r in rows if t0 + 0.5 * (t1 - t0) <= t <= t1]
+        sm_mhz = [float(r.split(",")[0]) for r in tail if r.split(",")[0].strip().replace(".", "").isdigit()]
+        pw = [float(r.split(",")[2]) for r in tail if r.split(",")[2].strip().replace(".", "").isdigit()]
         res[name] = {"first10_ms": [round(x, 4) for x in ts[:10]], "median_first50": statistics.median(ts[:50]),
-                     "median_last100": statistics.median(ts[-100:]), "samples": smp[::max(1, len(smp) // 12)]}
+                     "median_last100": statistics.median(ts[-100:]), "samples": smp[::max(1, len(smp) // 12)],
+                     "sm_mhz_median_2nd_half": statistics.median(sm_mhz) if sm_mhz else None,
+                     "power_w_median_2nd_half": statistics.median(pw) if pw else None}
     stop.set()
     nb = out.numel() * 4
     for k in res:
         res[k]["gbs_first50"] = nb / res[k]["median_first50"] / 1e6
         res[k]["gbs_last100"] = nb / res[k]["median_last100"] / 1e6
     os.makedirs("gpurun_out", exist_ok=True)
-    with open("gpurun_out/sustained.json", "w") as f:
+    with open(f"gpurun_out/sustained{'_' + a.tag if a.tag else ''}.json", "w") as f:
         json.dump(res, f, indent=1)
-    print(json.dumps({k: {x: v[x] for x in ("median_first50", "median_last100", "gbs_first50", "gbs_last100")} for k, v in res.items()}, indent=1))
-    for k in res:
-        print(k, res[k]["samples"])
+    for k, v in res.items():
+        print(f"{a.tag or '-'} {k}: burst {v['gbs_first50']:.0f} GB/s, last100 {v['gbs_last100']:.0f} GB/s "
+              f"({v['median_last100']:.4f} ms), sm {v['sm_mhz_median_2nd_half']} MHz, {v['power_w_median_2nd_half']} W")
 
 
 if __name__ == "__main__":
