@@ -55,7 +55,7 @@ int main(int argc, char **argv)
     cudaMemcpy(dpts, h, (size_t)n * 3 * sizeof(float), cudaMemcpyHostToDevice);
 
     smap_stats st;
-    CHECK(smap_run(plan, SMAP_PAYLOAD_EDM, dpts, 0.0f, dout, nb, SMAP_RUN_XOR, NULL));
+    CHECK(smap_run(plan, SMAP_PAYLOAD_EDM, dpts, (size_t)n * 3 * sizeof(float), 0.0f, dout, nb, SMAP_RUN_XOR, NULL));
     CHECK(smap_stats_fetch(plan, &st));
 
     /* verify one distance through smap_locate, recomputed here in the stated fp32 order (E17) */

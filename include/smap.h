@@ -27,6 +27,10 @@
  *   - Ownership: the caller owns `points`, `out` and the stream; a plan owns
  *     only its own scratch (result block, fp64 partials, staging buffers).
  *   - A plan may be used from one stream at a time (not re-entrant).
+ *   - Devices: a plan lives on the device it was planned for (smap_plan_desc.device);
+ *     every entry point taking a plan makes that device current for the call and
+ *     restores the caller's current device before returning (also on errors).
+ *     Streams and buffers passed with a plan must belong to its device.
  */
 #ifndef SMAP_H
 #define SMAP_H
@@ -38,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SMAP_ABI_VERSION 1
+#define SMAP_ABI_VERSION 2   /* 2: smap_run / smap_run_host take the points buffer size */
 
 typedef enum {
     SMAP_OK = 0,
@@ -120,7 +124,8 @@ typedef struct smap_plan_s *smap_plan_t;
 
 typedef struct {
     int     m;            /* 2 or 3 */
-    int64_t n;            /* elements per side, any n in [m, 2^30]: the grid is built for
+    int64_t n;            /* elements per side, any n in [m, 2^30] (m=3: every count of the plan, e.g.
+                             8 * C(n,3), must fit in 64 bits, i.e. n <= ~2.6e6): the grid is built for
                              n' = 2^ceil(log2 n) and elements with an index >= n are filtered
                              ("approach n from above"); n' != n needs shard_count 1
                              and the canonical layout */
@@ -175,7 +180,8 @@ typedef struct {
 
 /* Validate `d`, derive the grid and the closed forms, and allocate the plan's
  * scratch on d->device.  Host math plus small cudaMalloc's; launches nothing.
- * SMAP_E_INVALID: m not in {2,3}; n outside [m, 2^30]; rho not a power of two;
+ * SMAP_E_INVALID: m not in {2,3}; n outside [m, 2^30]; a plan count (volume x 8 bytes,
+ * launched threads, dump bytes) that does not fit in 64 bits; rho not a power of two;
  * N = n'/rho too small (m=2: N >= 2; m=3 lambda: N >= 8, BB: N >= 1), with
  * n' = 2^ceil(log2 n) (2^ceil(log2 (n+2)) for m=3 inclusive); rho outside the
  * granularity's range; shard_count not a power of two or not dividing N/2, or
@@ -193,28 +199,34 @@ smap_status smap_plan_query(smap_plan_t p, smap_stats *st);
 smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes);
 
 /* Run payload pl over the plan's grid, asynchronously on `stream`
- * (cudaStream_t; NULL = legacy default stream).
- *   points: DEVICE pointer to n x 3 fp32 (x,y,z) array-of-structs; required
- *           for EDM/ATM/TC, ignored otherwise (may be NULL).
- *   param:  ATM: eps^2 (softening); TC: R (distance threshold); else ignored.
- *   out:    DEVICE pointer of >= smap_out_bytes bytes, or NULL for ATM/TC/EMPTY.
- *   flags:  SMAP_RUN_* bits.
+ * (cudaStream_t of the plan's device; NULL = legacy default stream).
+ *   points:       DEVICE pointer to n x 3 fp32 (x,y,z) array-of-structs, 4-byte
+ *                 aligned; required for EDM/ATM/TC, ignored otherwise (may be NULL).
+ *   points_bytes: size of the points buffer; must be >= n * 12 when points are used.
+ *   param:        ATM: eps^2 (softening); TC: R (distance threshold); else ignored.
+ *   out:          DEVICE pointer of >= smap_out_bytes bytes, or NULL for ATM/TC/EMPTY;
+ *                 16-byte aligned for SMAP_LAYOUT_TILES plans and MAP_DUMP (16-B vector
+ *                 stores), else aligned to the element (4 B; 8 B for uint64 / THREAD_DUMP).
+ *   flags:        SMAP_RUN_* bits.
  * The plan's result block is zeroed on the stream first; results are read with
- * smap_stats_fetch.  SMAP_E_INVALID: payload/m mismatch, missing points/out,
- * out_bytes too small, THREAD_DUMP with TILE granularity.
+ * smap_stats_fetch.  SMAP_E_INVALID (nothing launched): payload/m mismatch,
+ * missing points/out, points_bytes or out_bytes too small, a misaligned buffer,
+ * THREAD_DUMP with TILE granularity.
  * SMAP_E_UNSUPPORTED: ATM / INDEX_WRITE_ATM with TILE rho > 32; ATM / TC /
  * INDEX_WRITE_ATM on an inclusive plan. */
-smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float param,
+smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
                      void *out, size_t out_bytes, uint32_t flags, void *stream);
 
-/* End-to-end variant with a HOST point array: copies host_points (n x 3 fp32;
- * pinned memory recommended) to the plan's device staging buffer on `stream`,
- * runs like smap_run, reduces the result on the device (smap_result_reduce),
- * copies the 56-byte smap_result back to host and synchronises the stream;
- * *stats (required) receives the results.  `out` stays a DEVICE buffer (the
- * packed outputs are consumed on the device). */
-smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, float param,
-                          void *out, size_t out_bytes, uint32_t flags, void *stream,
+/* End-to-end variant with a HOST point array: copies host_points (n x 3 fp32,
+ * points_bytes >= n * 12; pinned memory recommended) to the plan's device
+ * staging buffer on `stream`, runs like smap_run, reduces the result on the
+ * device (smap_result_reduce), copies the 56-byte smap_result back to host and
+ * synchronises the stream; *stats (required) receives the results.  `out`
+ * stays a DEVICE buffer: the packed outputs (8.59 GB for C2) are consumed on
+ * the device and are NOT copied to the host -- the host receives the
+ * reductions (count, checksums / xor, ATM sum, TC count). */
+smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, size_t points_bytes,
+                          float param, void *out, size_t out_bytes, uint32_t flags, void *stream,
                           smap_stats *stats);
 
 /* Synchronise the stream of the last smap_run and copy its results (a few
@@ -246,9 +258,10 @@ smap_status smap_result_combine(const void *records, int count, void *dst, void 
  * *shard = the shard rank that writes it, *pos = its position in that shard's
  * `out` array (SMAP_LAYOUT_ROWS: the packed rank in the full-size array;
  * SMAP_LAYOUT_TILES: the position in the shard-local tile-blocked array).
- * Host only, O(1) (lambda2^-1 via b = 2^floor(log2(I xor J)), q = I >> (log2 b + 1)).
- * SMAP_E_INVALID for an element outside the domain; SMAP_E_UNSUPPORTED for m=3 with
- * shard_count > 1. */
+ * Host only, O(1) (lambda2^-1 via b = 2^floor(log2(I xor J)), q = I >> (log2 b + 1);
+ * lambda3^-1 via b = 2^floor(log2(I xor K)), q = I >> (log2 b + 1), inside iff J - I < b),
+ * sharded plans included (the owner shard is omega_x / W).  BELOW plans: the E29 layout,
+ * piece lookup + closed form.  SMAP_E_INVALID for an element outside the domain. */
 smap_status smap_locate(smap_plan_t p, const int64_t *e, int *shard, uint64_t *pos);
 
 /* Useful-element count V of a domain: C(n,2), n(n+1)/2 or C(n,3).  Host only. */

@@ -64,8 +64,9 @@ _SIGS = {
     "smap_plan": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(_P)]),
     "smap_plan_query": (C.c_int, [_P, C.POINTER(Stats)]),
     "smap_out_bytes": (C.c_int, [_P, C.c_int, C.POINTER(C.c_size_t)]),
-    "smap_run": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_size_t, C.c_uint32, _P]),
-    "smap_run_host": (C.c_int, [_P, C.c_int, _P, C.c_float, _P, C.c_size_t, C.c_uint32, _P, C.POINTER(Stats)]),
+    "smap_run": (C.c_int, [_P, C.c_int, _P, C.c_size_t, C.c_float, _P, C.c_size_t, C.c_uint32, _P]),
+    "smap_run_host": (C.c_int, [_P, C.c_int, _P, C.c_size_t, C.c_float, _P, C.c_size_t, C.c_uint32, _P,
+                                C.POINTER(Stats)]),
     "smap_stats_fetch": (C.c_int, [_P, C.POINTER(Stats)]),
     "smap_result_reduce": (C.c_int, [_P, _P, _P]),
     "smap_result_combine": (C.c_int, [_P, C.c_int, _P, _P]),
@@ -105,11 +106,13 @@ def smap_volume(m: int, n: int, diag: str = "strict") -> int:
 
 
 class Plan:
-    """Owns an smap_plan_t; see smap_plan."""
+    """Owns an smap_plan_t; see smap_plan.  `device` is the CUDA ordinal the
+    plan lives on (resolved from the current device when planned with -1)."""
 
-    def __init__(self, handle, desc: PlanDesc):
+    def __init__(self, handle, desc: PlanDesc, device: int):
         self.handle = handle
         self.desc = desc
+        self.device = device
 
     @property
     def m(self): return self.desc.m
@@ -133,7 +136,11 @@ def smap_plan(m: int, n: int, rho: int, map: str = "lambda", diag: str = "strict
                  ORDER[order], LAYOUT[layout])
     h = _P()
     _check(_lib.smap_plan(C.byref(d), C.byref(h)))
-    return Plan(h, d)
+    dev = device
+    if device == -1:
+        import torch
+        dev = torch.cuda.current_device()
+    return Plan(h, d, dev)
 
 
 def smap_destroy(plan: Plan):
@@ -163,6 +170,8 @@ def smap_out_bytes(plan: Plan, payload: str) -> int:
 
 
 def _ptr(x):
+    """Address of a ctypes-compatible buffer: an int (raw pointer), a torch
+    tensor or a numpy array, or None."""
     if x is None:
         return None
     if isinstance(x, int):
@@ -194,21 +203,61 @@ def _stream(stream):
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
+def _device_buffer(plan: Plan, x, what: str, nbytes=None, fp32_points=False):
+    """(pointer, bytes) of a DEVICE buffer for smap_run: a contiguous torch CUDA
+    tensor on the plan's device, or a raw device pointer (int) with an explicit
+    byte count.  Host arrays are refused (use smap_run_host)."""
+    if x is None:
+        return None, 0
+    if isinstance(x, int):
+        if nbytes is None:
+            raise ValueError(f"{what}: a raw pointer needs an explicit {what}_bytes")
+        return x, int(nbytes)
+    if not hasattr(x, "is_cuda"):
+        raise TypeError(f"{what} must be a CUDA tensor (or a raw device pointer); host arrays go through smap_run_host")
+    if not x.is_cuda:
+        raise ValueError(f"{what} is a host tensor; smap_run takes device buffers (use smap_run_host for host points)")
+    if x.device.index != plan.device:
+        raise ValueError(f"{what} is on cuda:{x.device.index}, the plan on cuda:{plan.device}")
+    if not x.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    if fp32_points:
+        import torch
+        if x.dtype != torch.float32 or x.numel() < 3 * plan.n:
+            raise ValueError(f"{what} must be float32 with at least n x 3 = {3 * plan.n} elements "
+                             f"(got {x.dtype}, {x.numel()})")
+    return x.data_ptr(), _nbytes(x) if nbytes is None else int(nbytes)
+
+
 def smap_run(plan: Plan, payload: str, points=None, param: float = 0.0, out=None, flags: int = 0,
-             stream=None):
+             stream=None, points_bytes=None, out_bytes=None):
     """Asynchronous launch on `stream` (default: torch's current stream).
-    points/out are DEVICE tensors (or raw device pointers with out_bytes implied)."""
-    _check(_lib.smap_run(plan.handle, PAYLOAD[payload], _ptr(points), float(param), _ptr(out),
-                         _nbytes(out) if not isinstance(out, int) else (1 << 62), flags, _stream(stream)))
+    points / out: contiguous CUDA tensors on the plan's device (points float32,
+    n x 3), or raw device pointers with explicit points_bytes / out_bytes."""
+    pp, pb = _device_buffer(plan, points, "points", points_bytes, fp32_points=True)
+    op, ob = _device_buffer(plan, out, "out", out_bytes)
+    _check(_lib.smap_run(plan.handle, PAYLOAD[payload], pp, pb, float(param), op, ob, flags, _stream(stream)))
 
 
 def smap_run_host(plan: Plan, payload: str, host_points=None, param: float = 0.0, out=None, flags: int = 0,
-                  stream=None) -> dict:
-    """End-to-end call with a HOST point array (copied H2D inside), results
-    copied back to host; synchronous.  `out` stays a device tensor."""
+                  stream=None, out_bytes=None) -> dict:
+    """End-to-end call with a HOST point array (float32 n x 3, numpy or a CPU
+    tensor, pinned recommended; copied H2D inside), results copied back to
+    host; synchronous.  `out` stays a device tensor: the packed outputs are
+    consumed on the device, only the 56-byte result record comes back."""
+    hp, hb = None, 0
+    if host_points is not None:
+        if getattr(host_points, "is_cuda", False):
+            raise ValueError("host_points is a CUDA tensor; use smap_run for device points")
+        import numpy as np
+        a = host_points.numpy() if hasattr(host_points, "numpy") else host_points
+        if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags.c_contiguous or a.size < 3 * plan.n:
+            raise ValueError("host_points must be a contiguous float32 array with at least n x 3 elements")
+        hp, hb = _ptr(host_points), a.nbytes
+    op, ob = _device_buffer(plan, out, "out", out_bytes)
     st = Stats()
-    _check(_lib.smap_run_host(plan.handle, PAYLOAD[payload], _ptr(host_points), float(param), _ptr(out),
-                              _nbytes(out), flags, _stream(stream), C.byref(st)))
+    _check(_lib.smap_run_host(plan.handle, PAYLOAD[payload], hp, hb, float(param), op, ob, flags, _stream(stream),
+                              C.byref(st)))
     return st.as_dict()
 
 

@@ -67,6 +67,25 @@ static smap_status cuda_fail(cudaError_t e, const char *where)
         if (e_ != cudaSuccess) return cuda_fail(e_, #call);       \
     } while (0)
 
+// Makes the plan's device current for the scope of one entry point and
+// restores the caller's device on every exit path.
+struct DevGuard {
+    int prev = -1;
+    bool switched = false;
+    cudaError_t enter(int dev)
+    {
+        cudaError_t e = cudaGetDevice(&prev);
+        if (e != cudaSuccess || prev == dev) return e;
+        e = cudaSetDevice(dev);
+        switched = e == cudaSuccess;
+        return e;
+    }
+    ~DevGuard()
+    {
+        if (switched) cudaSetDevice(prev);
+    }
+};
+
 static bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 static int ilog2(int64_t x) { int l = 0; while ((int64_t)1 << (l + 1) <= x) l++; return l; }
 
@@ -232,6 +251,17 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
     }
     uint64_t rm = 1;
     for (int k = 0; k < m; k++) rm *= (uint64_t)rho;
+    {   // every count and byte size of the plan must fit in 64 bits (m = 3 near n = 2^21 would wrap)
+        typedef unsigned __int128 u128;
+        const u128 Nn = (u128)n, lim = (u128)1 << 64;
+        const u128 V128 = m == 2 ? Nn * (Nn + 1) / 2 : (Nn + 2) * (Nn + 1) * Nn / 6;   // >= the domain volume
+        const u128 L128 = (u128)P.nblocks * rm;
+        if (V128 * 8 >= lim || L128 >= lim || (u128)P.nblocks * 16 >= lim) {
+            delete p;
+            return fail(SMAP_E_INVALID, "n = %lld is too large: the volume or the launched-thread count of "
+                                        "the plan exceeds 64 bits", (long long)n);
+        }
+    }
     p->launched = P.nblocks * rm;
     p->V = smap_volume(m, n, d->diag);
     p->useful = lam ? p->V / (uint64_t)G : p->V;
@@ -254,7 +284,8 @@ smap_status smap_plan(const smap_plan_desc *d, smap_plan_t *out)
         if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaGetDevice"); }
     }
     p->device = dev;
-    cudaError_t e = cudaSetDevice(dev);
+    DevGuard guard;                           // allocate on d->device, leave the caller's device current
+    cudaError_t e = guard.enter(dev);
     if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaSetDevice"); }
     int sms = 0;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -329,8 +360,8 @@ smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes)
     return SMAP_OK;
 }
 
-smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float param, void *out,
-                     size_t out_bytes, uint32_t flags, void *stream)
+smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
+                     void *out, size_t out_bytes, uint32_t flags, void *stream)
 {
     g_err.clear();
     if (!p) return fail(SMAP_E_INVALID, "smap_run: NULL plan");
@@ -345,7 +376,13 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     if (ipl == PL_EDM && (d.m != 2 || incl)) return fail(SMAP_E_INVALID, "EDM is defined on the m=2 strict domain");
     const bool atm = pl_atm(ipl);
     if ((atm || ipl == PL_TC) && d.m != 3) return fail(SMAP_E_INVALID, "ATM/TC are m=3 payloads");
-    if ((ipl == PL_EDM || atm || ipl == PL_TC) && !points) return fail(SMAP_E_INVALID, "payload needs points");
+    if (ipl == PL_EDM || atm || ipl == PL_TC) {
+        const size_t need_pts = (size_t)d.n * 3 * sizeof(float);
+        if (!points) return fail(SMAP_E_INVALID, "payload needs points");
+        if (points_bytes < need_pts)
+            return fail(SMAP_E_INVALID, "points buffer too small: need %zu bytes (n x 3 fp32), got %zu", need_pts, points_bytes);
+        if ((reinterpret_cast<uintptr_t>(points) & 3) != 0) return fail(SMAP_E_INVALID, "points not 4-byte aligned");
+    }
     if (atm && tile && d.m == 3 && d.rho > 32)
         return fail(SMAP_E_UNSUPPORTED, "ATM tiles are rho <= 32 (three rho x rho r^2 tables in shared memory)");
     if ((atm || ipl == PL_TC) && d.diag == SMAP_DIAG_INCLUSIVE)
@@ -355,6 +392,14 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     smap_out_bytes(p, pl, &need);
     if (need > 0 && (!out || out_bytes < need))
         return fail(SMAP_E_INVALID, "out buffer too small: need %zu bytes, got %zu", need, out ? out_bytes : (size_t)0);
+    if (need > 0) {
+        // the tile-blocked layouts are written with 16-B vector stores; the rows layout with
+        // element-sized stores (and 16-B records for MAP_DUMP)
+        const bool vec = d.layout == SMAP_LAYOUT_TILES || ipl == PL_MAPD;
+        const uintptr_t align = vec ? 16 : (ipl == PL_TDUMP || (pl_iw(ipl) && p->elem64)) ? 8 : 4;
+        if ((reinterpret_cast<uintptr_t>(out) & (align - 1)) != 0)
+            return fail(SMAP_E_INVALID, "out must be %u-byte aligned for this payload / layout", (unsigned)align);
+    }
     const bool csum_pl = pl_iw(ipl) || ipl == PL_EDM;
     const int cs = !csum_pl ? 0 : (flags & SMAP_RUN_CHECKSUM_MIX) ? 2 : (flags & SMAP_RUN_CHECKSUM) ? 1
                                  : (flags & SMAP_RUN_XOR) ? 3 : 0;
@@ -365,9 +410,8 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
         return fail(SMAP_E_INVALID, "reductions need rho^m to be a multiple of 32 (rho^m = %llu)", (unsigned long long)rm);
 
     cudaStream_t s = (cudaStream_t)stream;
-    int cur = -1;
-    CK(cudaGetDevice(&cur));
-    if (cur != p->device) CK(cudaSetDevice(p->device));
+    DevGuard guard;                           // the plan's device for this call; restored on every return
+    CK(guard.enter(p->device));
     const bool tc_bits = ipl == PL_TC && tile;
     const int64_t npad = (int64_t)p->P.N * d.rho;          // bitmap over the grid's index range
     if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)npad * (size_t)((npad + 31) / 32) * sizeof(uint32_t)));
@@ -411,7 +455,6 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, float 
     p->last_stream = s;
     p->last_launches = launches;
     p->ran = 1;
-    if (cur != p->device) cudaSetDevice(cur);
     return SMAP_OK;
 }
 
@@ -434,6 +477,8 @@ smap_status smap_stats_fetch(smap_plan_t p, smap_stats *st)
 {
     if (!p || !st) return fail(SMAP_E_INVALID, "smap_stats_fetch: NULL argument");
     if (!p->ran) return fail(SMAP_E_INVALID, "smap_stats_fetch before smap_run (or on a host-only plan)");
+    DevGuard guard;
+    CK(guard.enter(p->device));
     CK(cudaEventSynchronize(p->ev1));
     CK(cudaMemcpy(p->h_res, p->d_res, sizeof(Result), cudaMemcpyDeviceToHost));
     fill_stats(p, p->h_res, st);
@@ -662,6 +707,8 @@ smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream)
     if (p->device == SMAP_DEVICE_NONE) return fail(SMAP_E_INVALID, "smap_result_reduce on a host-only plan");
     if ((reinterpret_cast<uintptr_t>(dst) & 7) != 0) return fail(SMAP_E_INVALID, "smap_result_reduce: dst not 8-byte aligned");
     if (!p->ran) return fail(SMAP_E_INVALID, "smap_result_reduce before smap_run");
+    DevGuard guard;
+    CK(guard.enter(p->device));
     cudaError_t e = launch_result_reduce(p->d_res, reinterpret_cast<smap_result *>(dst), (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "result reduce launch");
     return SMAP_OK;
@@ -681,20 +728,27 @@ smap_status smap_result_combine(const void *records, int count, void *dst, void 
     return SMAP_OK;
 }
 
-smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, float param, void *out,
-                          size_t out_bytes, uint32_t flags, void *stream, smap_stats *stats)
+smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_points, size_t points_bytes, float param,
+                          void *out, size_t out_bytes, uint32_t flags, void *stream, smap_stats *stats)
 {
+    g_err.clear();
     if (!p || !stats) return fail(SMAP_E_INVALID, "smap_run_host: NULL argument");
     if (p->device == SMAP_DEVICE_NONE) return fail(SMAP_E_INVALID, "smap_run_host on a host-only plan");
     cudaStream_t s = (cudaStream_t)stream;
+    DevGuard guard;                           // staging buffers, kernels and copies on the plan's device
+    CK(guard.enter(p->device));
     const float *dev_pts = nullptr;
+    size_t dev_bytes = 0;
     if (host_points) {
         const size_t bytes = (size_t)p->d.n * 3 * sizeof(float);
+        if (points_bytes < bytes)
+            return fail(SMAP_E_INVALID, "host points buffer too small: need %zu bytes (n x 3 fp32), got %zu", bytes, points_bytes);
         if (!p->d_stage) CK(cudaMalloc(&p->d_stage, bytes));
         CK(cudaMemcpyAsync(p->d_stage, host_points, bytes, cudaMemcpyHostToDevice, s));
         dev_pts = p->d_stage;
+        dev_bytes = bytes;
     }
-    smap_status st = smap_run(p, pl, dev_pts, param, out, out_bytes, flags, stream);
+    smap_status st = smap_run(p, pl, dev_pts, dev_bytes, param, out, out_bytes, flags, stream);
     if (st != SMAP_OK) return st;
     if (!p->d_rec) CK(cudaMalloc(&p->d_rec, sizeof(smap_result)));
     if (!p->h_rec) CK(cudaMallocHost(&p->h_rec, sizeof(smap_result)));
@@ -714,6 +768,8 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
 void smap_destroy(smap_plan_t p)
 {
     if (!p) return;
+    DevGuard guard;
+    if (p->device >= 0) guard.enter(p->device);
     if (p->d_res) cudaFree(p->d_res);
     if (p->h_res) cudaFreeHost(p->h_res);
     if (p->d_partials) cudaFree(p->d_partials);

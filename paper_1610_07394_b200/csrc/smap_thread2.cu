@@ -29,7 +29,6 @@ __global__ void __launch_bounds__(1024) k_thread2(Params P)
     if (!LAM && b.cls == 4 && PL != PL_TDUMP) return;   // BB: whole block outside -> exit
 
     uint32_t i, j;
-    uint32_t si = 0, li = ty, sj = 1, lj = tx;    // (slot, local) of i and j; slot 0/1 = row/column block
     bool valid;
     if (!LAM) {
         i = b.I * rho + ty; j = b.J * rho + tx;
@@ -37,16 +36,14 @@ __global__ void __launch_bounds__(1024) k_thread2(Params P)
     } else if (b.cls == 0) {
         i = b.I * rho + ty; j = b.J * rho + tx; valid = true;
     } else if (b.cls == 1) {              // D1 = J keeps tx < ty; D2 = I point-reflected keeps tx > ty
-        if (tx < ty) { i = b.J * rho + ty;           j = b.J * rho + tx; sj = 0; }
-        else         { i = b.I * rho + rho - 1 - ty; j = b.I * rho + rho - 1 - tx; si = 1; li = rho - 1 - ty; lj = rho - 1 - tx; }
+        if (tx < ty) { i = b.J * rho + ty;           j = b.J * rho + tx; }
+        else         { i = b.I * rho + rho - 1 - ty; j = b.I * rho + rho - 1 - tx; }
         valid = tx != ty;
     } else {                              // inclusive diagonal block
-        i = b.J * rho + ty; j = b.J * rho + tx; valid = tx <= ty; sj = 0;
+        i = b.J * rho + ty; j = b.J * rho + tx; valid = tx <= ty;
     }
     valid = valid && i < (uint32_t)P.n;     // padded grid: rows i >= n are filtered out
     const uint64_t p = INCL ? rank2i(i, j) : rank2s(i, j);
-
-    (void)si; (void)li; (void)sj; (void)lj;   // (slot, local) coordinates: kept for staged variants
 
     if (PL == PL_TDUMP) {
         reinterpret_cast<uint64_t *>(P.out)[bid * rho * rho + ty * rho + tx] = valid ? p : ~0ull;

@@ -53,6 +53,29 @@ def main():
                 sm.smap_run(plan, pl, points=pts, param=1e-2, out=out, flags=sm.RUN_XOR)
                 sm.smap_stats_fetch(plan)
                 runs += 1
+    # the benchmarked EDM launches (VEC 16-B stores, warp-private staging reused across
+    # persistent tiles) with the timed step's reductions, plus the smap_run_host path
+    for n, rho, persistent in ((1024, 256, 0), (8192, 256, 1), (1024, 128, 0), (8192, 128, 1), (1000, 256, 0)):
+        pts = torch.from_numpy(workloads.points(n, 5)).cuda()
+        mp = "below" if n % rho else "lambda"
+        plan = sm.smap_plan(2, n, rho, map=mp, granularity="tile", layout="tiles", persistent=persistent)
+        out = sm.alloc_out(plan, "edm")
+        for flags in (sm.RUN_XOR, sm.RUN_CHECKSUM, 0):
+            sm.smap_run(plan, "edm", points=pts, out=out, flags=flags)
+            sm.smap_stats_fetch(plan)
+            runs += 1
+        sm.smap_run_host(plan, "edm", host_points=workloads.points(n, 5), out=out, flags=sm.RUN_XOR)
+        runs += 1
+    # the benchmarked C3 / C4 / C5 launches at reduced n
+    p3 = torch.from_numpy(workloads.points(512, 6)).cuda()
+    for kw, pl, n, param in ((workloads.BENCH_C3, "index_write_atm", 512, 1e-2), (workloads.BENCH_C4, "index_write", 2048, 0.0),
+                             (workloads.BENCH_C5, "tc", 512, 0.5)):
+        plan = sm.smap_plan(2 if pl == "index_write" else 3, n, **kw)
+        out = sm.alloc_out(plan, pl)
+        sm.smap_run(plan, pl, points=p3 if pl != "index_write" else None, param=param, out=out,
+                    flags=sm.RUN_XOR if pl != "tc" else 0)
+        sm.smap_stats_fetch(plan)
+        runs += 1
     torch.cuda.synchronize()
     print(f"sanitize cases: {runs} runs ok")
 

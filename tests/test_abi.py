@@ -2,6 +2,7 @@
 and validates arguments on the host without touching a GPU.  CPU only."""
 import ctypes
 import re
+import math
 import os
 
 import pytest
@@ -31,7 +32,7 @@ def test_header_is_plain_c():
 
 
 def test_abi_version(sm):
-    assert sm.smap_abi_version() == 1
+    assert sm.smap_abi_version() == 2
 
 
 def test_volume(sm):
@@ -122,6 +123,13 @@ def test_result_combine_and_locate_reject_bad_arguments(sm):
         sm.smap_locate(plan, 5, 7)                       # j > i: outside the strict domain
     with pytest.raises(sm.SmapError):
         sm.smap_run(plan, "edm")                         # host-only plan cannot run
+    # m=3 counts that would wrap 64 bits are refused at plan time (n = 2^22, 2^23)
+    for n3 in (1 << 22, 1 << 23, 1 << 30):
+        with pytest.raises(sm.SmapError) as e:
+            sm.smap_plan(3, n3, 64, granularity="tile", persistent=8, device=sm.DEVICE_NONE)
+        assert e.value.status == sm.E_INVALID and "64 bits" in str(e.value)
+    q = sm.smap_plan_query(sm.smap_plan(3, 1 << 21, 64, granularity="tile", device=sm.DEVICE_NONE))
+    assert q["useful_elems"] == math.comb(1 << 21, 3) and q["launched_threads"] == 3 * (1 << 21) ** 3 // 16
     plan3 = sm.smap_plan(3, 300, 8, map="below", granularity="tile", device=sm.DEVICE_NONE)
     with pytest.raises(sm.SmapError):
         sm.smap_locate(plan3, 3, 2, 1)                   # not i < j < k

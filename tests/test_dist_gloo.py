@@ -58,7 +58,7 @@ def test_host_only_plans_partition_volume(m, inc, n, rho, G):
     assert tot == V and len(blocks) == 1
     plan = sm.smap_plan(m, n, rho, diag=diag, device=sm.DEVICE_NONE)
     with pytest.raises(sm.SmapError):
-        sm.smap_run(plan, "index_write", out=0)
+        sm.smap_run(plan, "index_write", out=0, out_bytes=0)
 
 
 def test_shard_records_match_oracle_closed_form(orc):

@@ -311,6 +311,41 @@ def test_invalid_arguments(sm):
         sm.smap_run(plan, "edm", out=sm.alloc_out(plan, "edm"))   # no points
 
 
+def test_run_rejects_bad_buffers(sm):
+    """Boundary checks of smap_run (include/smap.h): short or misaligned
+    buffers are SMAP_E_INVALID before any launch; the binding refuses host
+    arrays, wrong dtypes and raw pointers without a size."""
+    import ctypes as C
+    n = 1024
+    plan = sm.smap_plan(2, n, 128, granularity="tile", layout="tiles")
+    pts = torch.from_numpy(workloads.points(n, 1)).cuda()
+    out = sm.alloc_out(plan, "edm")
+    with pytest.raises(sm.SmapError) as e:                      # one point short (the r01 initcheck case)
+        sm.smap_run(plan, "edm", points=pts.data_ptr(), points_bytes=(n - 1) * 12, out=out)
+    assert e.value.status == sm.E_INVALID and "points" in str(e.value)
+    big = torch.empty(out.numel() + 4, dtype=torch.float32, device="cuda")
+    with pytest.raises(sm.SmapError) as e:                      # 4-B aligned out on a 16-B vector-store layout
+        sm.smap_run(plan, "edm", points=pts, out=big.data_ptr() + 4, out_bytes=out.numel() * 4)
+    assert e.value.status == sm.E_INVALID and "aligned" in str(e.value)
+    with pytest.raises(TypeError):                              # host arrays belong to smap_run_host
+        sm.smap_run(plan, "edm", points=workloads.points(n, 1), out=out)
+    with pytest.raises(ValueError):
+        sm.smap_run(plan, "edm", points=pts.double(), out=out)
+    with pytest.raises(ValueError):
+        sm.smap_run(plan, "edm", points=pts[: n // 2], out=out)
+    with pytest.raises(ValueError):
+        sm.smap_run(plan, "edm", points=pts, out=out.data_ptr())   # raw pointer without out_bytes
+    with pytest.raises(ValueError):
+        sm.smap_run_host(plan, "edm", host_points=pts, out=out)   # device tensor given as host points
+    with pytest.raises(sm.SmapError):
+        sm._lib.smap_run_host(plan.handle, sm.PAYLOAD["edm"], C.c_void_p(workloads.points(n, 1).ctypes.data),
+                              12 * n - 12, 0.0, C.c_void_p(out.data_ptr()), out.numel() * 4, 0, None,
+                              C.byref(sm.Stats())) and sm._check(sm.E_INVALID)
+    # the plan still runs after the rejected calls
+    sm.smap_run(plan, "edm", points=pts, out=out, flags=sm.RUN_XOR)
+    assert sm.smap_stats_fetch(plan)["count"] == n * (n - 1) // 2
+
+
 # ---------------------------------------------------------------- m=3 tiles of 64 (TC / index write / cover)
 @pytest.mark.parametrize("map_", ["lambda", "bb"])
 def test_tile64_m3(sm, orc, map_):

@@ -30,6 +30,12 @@ CONFIGS = {
 }
 
 
+#: supplementary C5 scaling workload ("a supplementary run with more
+#: work as scaling evidence"): the same triple correlation at n = 8192 (64x the
+#: triples of C5); not a BASELINE config, reported beside C5 only
+SEED_C5X = 161007397
+C5X = dict(m=3, n=8192, seed=SEED_C5X, R=0.5, desc="C5 at n=8192 (supplementary scaling run)")
+
 #: launch configurations bench.py times (parity-tested at full size in
 #: tests/test_gpu_fullsize.py).  Keys are smap_plan keyword arguments.
 BENCH_EDM = dict(rho=256, granularity="tile", map="lambda", layout="tiles")
@@ -42,6 +48,13 @@ BENCH_M3_VARIANTS = [BENCH_M3, dict(rho=8, granularity="thread", map="lambda")]
 BENCH_C3 = dict(rho=32, granularity="tile", map="lambda", layout="tiles")   # fused index write + ATM (E26)
 BENCH_C4 = dict(rho=128, granularity="tile", map="lambda", layout="tiles")
 BENCH_C5 = dict(rho=64, granularity="tile", map="lambda", persistent=8)   # TC: 64-bit predicate rows, 8 CTAs/SM
+
+
+def sharded_launch(name: str, G: int) -> dict:
+    """smap_plan keyword arguments of config `name`'s product launch on one of
+    G omega_x shards (bench.py configs_sharded)."""
+    base = {"C2": BENCH_EDM, "C3": BENCH_C3, "C4": BENCH_C4, "C5": BENCH_C5, "C5X": BENCH_C5}[name]
+    return dict(base)
 
 
 def points(n: int, seed: int) -> np.ndarray:
