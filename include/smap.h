@@ -275,6 +275,43 @@ const char *smap_last_error(void);
 
 int smap_abi_version(void);
 
+/* ---- Volume analysis of recursive orthotope sets (host only) ----------
+ * The paper's analysis beyond the two maps: a set S_n^m of orthotopes built with scaling
+ * factor r and arity beta, V(S_n^m) = (r n)^m + beta V(S_{r n}^m), whose
+ * closed form is (n^m - beta^{log_{1/r} n}) / (1/r^m - beta) (Eq. generic-m);
+ * r = 1/2, beta = 2 gives lambda2's n(n-1)/2 and lambda3's (n^3 - n)/6, beta = 3 the
+ * arity-3 tetrahedral set (n^3 - 3^{log2 n})/5 (reading E8).  Readings E30
+ * (r*) and E31 (n0) in DESIGN.md. */
+
+/* V(S_n^m) by the recurrence, V(1) = 0, for r = 1/r_den and n a power of r_den; exact
+ * (128-bit intermediates).  SMAP_E_INVALID: m outside [1,16], beta < 1, r_den < 2, n not
+ * a power of r_den, or a result >= 2^64. */
+smap_status smap_recursive_volume(int m, uint64_t n, int beta, int r_den, uint64_t *vol);
+
+/* The same by the closed form of Eq. generic-m (beta = r_den^m: the degenerate sum
+ * k (n/r_den)^m); same errors. */
+smap_status smap_recursive_volume_closed(int m, uint64_t n, int beta, int r_den, uint64_t *vol);
+
+/* lim_{n->inf} V(S_n^m) / V(Delta_n^m) - 1 = m! / (1/r^m - beta) - 1;
+ * +inf when 1/r^m <= beta (the set grows faster than n^m); NaN for r outside (0,1). */
+double smap_alpha_limit(int m, double r, int beta);
+
+/* r* = (m! + beta)^{-1/m}: the scaling meeting the constraint 1/r^m - beta = m! (
+ * the printed r = 1/(m^{-1/m}) is > 1, reading E30). */
+double smap_r_star(int m, int beta);
+
+/* n0 (reading E31): the smallest n in [2, n_max] such that the continuous
+ * V(S_{n'}^m) >= V(Delta^m_{n'-1}) = C(n'+m-2, m) for every n' in [n, n_max]; *n0 = 0 when
+ * the set does not cover at n_max.  *ratio_at_nmax (optional) = V(S)/V(Delta_{n-1}) there.
+ * SMAP_E_INVALID: bad m / r / beta, n_max outside [2, 2^24]. */
+smap_status smap_find_n0(int m, double r, int beta, uint64_t n_max, uint64_t *n0, double *ratio_at_nmax);
+
+/* The paper's open optimisation for one beta: the smallest r -- i.e. the least
+ * extra volume m!/(1/r^m - beta) - 1 -- whose set covers Delta^m_{n-1} for every n in
+ * [n0, n_max] (continuous model, bisection between r* and the r of 1/r^m - beta = 1).
+ * SMAP_E_UNSUPPORTED if even 1/r^m - beta = 1 does not cover; n_max <= 2^20. */
+smap_status smap_r_cover(int m, int beta, uint64_t n0, uint64_t n_max, double *r);
+
 /* MAP_DUMP record per grid block (THREAD) or tile (TILE), in launch order:
  *   int32 {x0, x1, x2, cls}
  * m=2 lambda: cls 0 off-diagonal block (x0,x1) = (J,I) = lambda2(w);

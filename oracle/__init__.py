@@ -45,6 +45,8 @@ _SIGS = {
     "or_vs2_recurrence": (u64, [u64]),
     "or_vs3_recurrence": (u64, [u64]),
     "or_vs3_arity3_recurrence": (u64, [u64]),
+    "or_vsm_recurrence": (u64, [i32, u64, u64, u64]),
+    "or_vsm_alpha": (f64, [i32, u64, u64, u64]),
     "or_floor_log2": (i32, [u64]),
     "or_lambda2": (i32, [u64, u64, P, P]),
     "or_rec2": (i32, [u64, u64, u64, P, P]),
@@ -119,6 +121,8 @@ def bb_alpha(m, n): return lib().or_bb_alpha(m, n)
 def vs2(n): return lib().or_vs2_recurrence(n)
 def vs3(n): return lib().or_vs3_recurrence(n)
 def vs3_arity3(n): return lib().or_vs3_arity3_recurrence(n)
+def vsm(m, n, beta=2, rden=2): return lib().or_vsm_recurrence(m, n, beta, rden)
+def vsm_alpha(m, n, beta=2, rden=2): return lib().or_vsm_alpha(m, n, beta, rden)
 def floor_log2(y): return lib().or_floor_log2(y)
 def domain_volume(m, inclusive, n): return lib().or_domain_volume(m, int(inclusive), n)
 

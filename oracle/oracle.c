@@ -117,6 +117,36 @@ uint64_t or_vs3_arity3_recurrence(uint64_t n)
     return (n / 2) * (n / 2) * (n / 2) + 3 * or_vs3_arity3_recurrence(n / 2);
 }
 
+/* the general recursive set V(S_n^m) = (r n)^m + beta V(S_{r n}^m), r = 1/rden,
+ * written top-down exactly as printed (V(S_1) = 0); UINT64_MAX when n is not a power of
+ * rden or a value overflows 64 bits.  r = 1/2, beta = 2 is lambda2's set (m = 2) and the
+ * two-branch tetrahedral set (m = 3); beta = 3, m = 3 the arity-3 set. */
+uint64_t or_vsm_recurrence(int m, uint64_t n, uint64_t beta, uint64_t rden)
+{
+    if (n <= 1) return n == 1 ? 0 : UINT64_MAX;
+    if (n % rden != 0) return UINT64_MAX;
+    uint64_t sub = or_vsm_recurrence(m, n / rden, beta, rden);
+    if (sub == UINT64_MAX) return UINT64_MAX;
+    u128 cube = 1;
+    for (int i = 0; i < m; i++) {
+        cube *= (u128)(n / rden);
+        if (cube >> 64) return UINT64_MAX;
+    }
+    u128 v = cube + (u128)beta * sub;
+    return (v >> 64) ? UINT64_MAX : (uint64_t)v;
+}
+
+/* the extra volume at a finite n, V(S_n^m) / V(Delta_n^m) - 1, with V(Delta_n^m)
+ * = C(n+m-1, m) by counting in long double (pins the limit numerically at large n) */
+double or_vsm_alpha(int m, uint64_t n, uint64_t beta, uint64_t rden)
+{
+    uint64_t vs = or_vsm_recurrence(m, n, beta, rden);
+    if (vs == UINT64_MAX) return NAN;
+    long double vd = 1.0L;
+    for (int i = 0; i < m; i++) vd = vd * (long double)(n + i) / (long double)(i + 1);
+    return (double)((long double)vs / vd - 1.0L);
+}
+
 /* ======================================================================
  * L2 -- block-space maps
  * ====================================================================== */

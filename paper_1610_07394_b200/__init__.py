@@ -75,6 +75,12 @@ _SIGS = {
     "smap_destroy": (None, [_P]),
     "smap_last_error": (C.c_char_p, []),
     "smap_abi_version": (C.c_int, []),
+    "smap_recursive_volume": (C.c_int, [C.c_int, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
+    "smap_recursive_volume_closed": (C.c_int, [C.c_int, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
+    "smap_alpha_limit": (C.c_double, [C.c_int, C.c_double, C.c_int]),
+    "smap_r_star": (C.c_double, [C.c_int, C.c_int]),
+    "smap_find_n0": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
+    "smap_r_cover": (C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -293,6 +299,37 @@ def result_dict(rec) -> dict:
     d = dict(zip(RESULT_FIELDS[:6], (int(x) for x in u[:6])))
     d["sum"] = float(a[6:7].view(np.float64)[0])
     return d
+
+
+# ------------------------------------------------------------------ volume analysis (host only, NEXT-4)
+def smap_recursive_volume(m: int, n: int, beta: int = 2, r_den: int = 2, closed: bool = False) -> int:
+    """V(S_n^m) of the recursive orthotope set with r = 1/r_den and arity beta
+    (recurrence, or the closed form of Eq. generic-m with closed=True)."""
+    v = C.c_uint64()
+    fn = _lib.smap_recursive_volume_closed if closed else _lib.smap_recursive_volume
+    _check(fn(m, n, beta, r_den, C.byref(v)))
+    return v.value
+
+
+def smap_alpha_limit(m: int, r: float = 0.5, beta: int = 2) -> float:
+    return _lib.smap_alpha_limit(m, r, beta)
+
+
+def smap_r_star(m: int, beta: int = 2) -> float:
+    return _lib.smap_r_star(m, beta)
+
+
+def smap_find_n0(m: int, r: float, beta: int, n_max: int) -> tuple:
+    """(n0 or None, V(S)/V(Delta_{n-1}) at n_max)."""
+    n0, ratio = C.c_uint64(), C.c_double()
+    _check(_lib.smap_find_n0(m, r, beta, n_max, C.byref(n0), C.byref(ratio)))
+    return (n0.value or None), ratio.value
+
+
+def smap_r_cover(m: int, beta: int, n0: int, n_max: int) -> float:
+    r = C.c_double()
+    _check(_lib.smap_r_cover(m, beta, n0, n_max, C.byref(r)))
+    return r.value
 
 
 # ------------------------------------------------------------------ torch conveniences

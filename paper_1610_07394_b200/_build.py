@@ -19,7 +19,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "smap")
 LIB = os.path.join(PKG, "libsmap.so")
 
-SOURCES = ["smap_api.cu", "smap_thread2.cu", "smap_thread3.cu", "smap_tile2.cu", "smap_tile3.cu"]
+SOURCES = ["smap_api.cu", "smap_thread2.cu", "smap_thread3.cu", "smap_tile2.cu", "smap_tile3.cu", "smap_analysis.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
               "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
