@@ -273,21 +273,23 @@ class Ctx:
 
 
 def shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps, warm=2):
-    """Per-rank device times of `reps` steps of one sharded config: kernel =
-    smap_run (events around it on the launching stream), step = smap_run +
-    smap_result_reduce + (G > 1) the all-gather of the records + combine.
-    Returns (median step ms, median kernel ms, combined record)."""
+    """Per-rank device times of `reps` steps of one sharded config.  The
+    rank's part of the step -- the payload kernels and the record reduction --
+    is one CUDA graph (smap_graph_capture: no host enqueue between its
+    kernels); step = graph + (G > 1) the all-gather of the 56-byte records +
+    the combine kernel.  Returns (median step ms, median graph ms, combined
+    record, kernels per step)."""
     torch, sm, s = ctx.torch, ctx.sm, ctx.stream
     rec = torch.zeros(7, dtype=torch.int64, device=ctx.dev)
     gathered = torch.zeros(ctx.G * 7, dtype=torch.int64, device=ctx.dev)
+    graph = sm.smap_graph_capture(plan, payload, points=pts, param=param, out=out, flags=flags, record=rec)
 
     def step(ka=None, kb=None):
         if ka is not None:
             ka.record(s)
-        sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags, stream=s)
+        sm.smap_graph_launch(graph, stream=s)
         if kb is not None:
             kb.record(s)
-        sm.smap_result_reduce(plan, rec, stream=s)
         if ctx.G > 1:
             ctx.dist.all_gather_into_tensor(gathered, rec)
             sm.smap_result_combine(gathered, ctx.G, rec, stream=s)
@@ -301,9 +303,10 @@ def shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps, warm=2):
         step(ka, kb)
         b.record(s)
     ctx.barrier()
-    step_ms = statistics.median(a.elapsed_time(b) for a, _, _, b in ev)
-    kern_ms = statistics.median(ka.elapsed_time(kb) for _, ka, kb, _ in ev)
-    return step_ms, kern_ms, ctx.sm.result_dict(rec)
+    step_ms = statistics.median(a.elapsed_time(b) for a, _, _, b in ev) if reps else 0.0
+    kern_ms = statistics.median(ka.elapsed_time(kb) for _, ka, kb, _ in ev) if reps else 0.0
+    launches = graph.launches + (1 if ctx.G > 1 else 0)
+    return step_ms, kern_ms, ctx.sm.result_dict(rec), launches
 
 
 def sharded_configs(ctx, golden):
@@ -322,13 +325,15 @@ def sharded_configs(ctx, golden):
         plan = sm.smap_plan(m, n, shard_rank=ctx.rank, shard_count=ctx.G, device=ctx.local, **launch)
         pts = torch.from_numpy(workloads.points(n, seed)).to(ctx.dev) if seed else None
         out = sm.alloc_out(plan, payload, device=ctx.dev)
-        flags = sm.RUN_XOR if payload != "tc" else 0
-        step_ms, kern_ms, _ = shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps)
+        # the step's fused reduction: count + xor for the index write (C4); count + the ATM sum
+        # for C3 (the xor of the ranks 0 .. V-1 is 0, so C3 skips it); count + tc for C5
+        flags = sm.RUN_XOR if payload == "index_write" else 0
+        step_ms, kern_ms, _, launches = shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps)
         step_max, kern_max = ctx.max_over_ranks(step_ms, kern_ms)
         (kern_min,) = ctx.min_over_ranks(kern_ms)
         # verification step (untimed): count + s0 (index writes; their xr of 0 .. V-1 is 0) / ATM sum / TC count
         vflags = sm.RUN_CHECKSUM if payload != "tc" else 0
-        _, _, rec = shard_step_timing(ctx, plan, payload, pts, param, out, vflags, 1, warm=0)
+        _, _, rec, _ = shard_step_timing(ctx, plan, payload, pts, param, out, vflags, 0, warm=1)
         g = golden[name]
         ok = rec["count"] == g["count"]
         if "s0" in g:
@@ -338,7 +343,8 @@ def sharded_configs(ctx, golden):
         if "tc" in g:
             ok = ok and rec["tc"] == g["tc"]
         V = g["count"]
-        e = {"launch": launch, "ms_per_step": round(step_max, 4), "kernel_ms_max": round(kern_max, 4),
+        e = {"launch": launch, "flags": flags, "kernels_per_step": launches,
+             "ms_per_step": round(step_max, 4), "kernel_ms_max": round(kern_max, 4),
              "kernel_ms_min": round(kern_min, 4), "kernel_max_over_min": round(kern_max / kern_min, 3),
              "elements_per_s": V / (step_max * 1e-3), "elements_per_s_kernel": V / (kern_max * 1e-3),
              "checked_vs_oracle": bool(ok)}

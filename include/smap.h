@@ -254,6 +254,26 @@ smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream);
  * misalignment or count < 1. */
 smap_status smap_result_combine(const void *records, int count, void *dst, void *stream);
 
+/* ---- CUDA graphs: one step without host enqueue gaps -------------------------------
+ * smap_graph_capture records one step of plan p -- the kernels of smap_run(p, pl, points,
+ * ..., flags) followed, when record != NULL, by smap_result_reduce(p, record) -- into a
+ * CUDA graph on a private stream and instantiates it (validation and lazily allocated
+ * scratch happen first, outside the capture; nothing runs).  smap_graph_launch replays it
+ * on `stream` (of the plan's device): the step's 1-4 kernels run back to back with no host
+ * work between them, which matters for steps of tens of microseconds (C3, C5).  Buffers
+ * (points, out, record) and the plan are bound at capture time: they must outlive the
+ * graph and not move.  Results of a replay are read from `record` (a device smap_result,
+ * 8-byte aligned); smap_stats_fetch / kernel_ms describe the last smap_run only.  Errors as
+ * smap_run; SMAP_E_CUDA if the capture or instantiation fails. */
+typedef struct smap_graph_s *smap_graph_t;
+smap_status smap_graph_capture(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
+                               void *out, size_t out_bytes, uint32_t flags, void *record, smap_graph_t *g);
+smap_status smap_graph_launch(smap_graph_t g, void *stream);
+/* kernels one replay launches (0 for NULL) */
+uint32_t smap_graph_launches(smap_graph_t g);
+/* NULL-safe; the plan is not destroyed */
+void smap_graph_destroy(smap_graph_t g);
+
 /* Where element e lives (m=2: e = {i, j}, j < i (<= i inclusive); m=3: e = {i, j, k}):
  * *shard = the shard rank that writes it, *pos = its position in that shard's
  * `out` array (SMAP_LAYOUT_ROWS: the packed rank in the full-size array;

@@ -75,6 +75,11 @@ _SIGS = {
     "smap_destroy": (None, [_P]),
     "smap_last_error": (C.c_char_p, []),
     "smap_abi_version": (C.c_int, []),
+    "smap_graph_capture": (C.c_int, [_P, C.c_int, _P, C.c_size_t, C.c_float, _P, C.c_size_t, C.c_uint32, _P,
+                                     C.POINTER(_P)]),
+    "smap_graph_launch": (C.c_int, [_P, _P]),
+    "smap_graph_launches": (C.c_uint32, [_P]),
+    "smap_graph_destroy": (None, [_P]),
     "smap_recursive_volume": (C.c_int, [C.c_int, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
     "smap_recursive_volume_closed": (C.c_int, [C.c_int, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
     "smap_alpha_limit": (C.c_double, [C.c_int, C.c_double, C.c_int]),
@@ -267,6 +272,45 @@ def smap_run_host(plan: Plan, payload: str, host_points=None, param: float = 0.0
     return st.as_dict()
 
 
+class Graph:
+    """Owns an smap_graph_t (one captured step of a plan); keeps the plan and
+    the bound buffers alive for as long as the graph exists."""
+
+    def __init__(self, handle, plan, keep):
+        self.handle = handle
+        self.plan = plan
+        self._keep = keep
+
+    @property
+    def launches(self) -> int:
+        return _lib.smap_graph_launches(self.handle)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.smap_graph_destroy(self.handle)
+                self.handle = None
+        except (TypeError, AttributeError):
+            pass
+
+
+def smap_graph_capture(plan: Plan, payload: str, points=None, param: float = 0.0, out=None, flags: int = 0,
+                       record=None, points_bytes=None, out_bytes=None) -> Graph:
+    """Capture one step (smap_run + smap_result_reduce into `record`, a device
+    tensor of 7 int64) into a CUDA graph; replay it with smap_graph_launch."""
+    pp, pb = _device_buffer(plan, points, "points", points_bytes, fp32_points=True)
+    op, ob = _device_buffer(plan, out, "out", out_bytes)
+    rp, _ = _device_buffer(plan, record, "record", None if record is None or not isinstance(record, int) else 56)
+    h = _P()
+    _check(_lib.smap_graph_capture(plan.handle, PAYLOAD[payload], pp, pb, float(param), op, ob, flags, rp,
+                                   C.byref(h)))
+    return Graph(h, plan, (points, out, record))
+
+
+def smap_graph_launch(graph: Graph, stream=None):
+    _check(_lib.smap_graph_launch(graph.handle, _stream(stream)))
+
+
 def smap_stats_fetch(plan: Plan) -> dict:
     st = Stats()
     _check(_lib.smap_stats_fetch(plan.handle, C.byref(st)))
@@ -361,6 +405,6 @@ def alloc_out(plan: Plan, payload: str, device="cuda", zero: bool = False):
 
 
 __all__ = ["smap_plan", "smap_plan_query", "smap_out_bytes", "smap_run", "smap_run_host", "smap_stats_fetch",
-           "smap_result_reduce", "smap_result_combine",
+           "smap_result_reduce", "smap_result_combine", "smap_graph_capture", "smap_graph_launch", "Graph",
            "smap_volume", "smap_destroy", "smap_last_error", "smap_abi_version", "Plan", "SmapError",
            "alloc_out", "exported_symbols", "RUN_CHECKSUM", "RUN_CHECKSUM_MIX", "RUN_XOR"]

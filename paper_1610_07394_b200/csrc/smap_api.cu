@@ -360,17 +360,27 @@ smap_status smap_out_bytes(smap_plan_t p, smap_payload pl, size_t *bytes)
     return SMAP_OK;
 }
 
-smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
-                     void *out, size_t out_bytes, uint32_t flags, void *stream)
+}  // extern "C"
+
+// One validated run: the launch arguments derived by run_prepare.
+struct RunArgs {
+    int ipl = 0, cs = 0;
+    bool tile = false, incl = false, atm = false, tc_bits = false;
+    int64_t npad = 0;
+    Params P;
+};
+
+// Validation and the plan's lazily allocated scratch (TC bitmap, ATM partials); the
+// plan's device must be current.  No device work is queued.
+static smap_status run_prepare(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
+                               void *out, size_t out_bytes, uint32_t flags, RunArgs *a)
 {
-    g_err.clear();
     if (!p) return fail(SMAP_E_INVALID, "smap_run: NULL plan");
     if (p->device == SMAP_DEVICE_NONE) return fail(SMAP_E_INVALID, "smap_run on a host-only plan");
     const int ipl = internal_pl(p, pl);
     if (ipl < 0) return fail(SMAP_E_INVALID, "unknown payload %d", (int)pl);
     const smap_plan_desc &d = p->d;
     const bool tile = d.granularity == SMAP_GRAN_TILE;
-    const bool lam = d.map == SMAP_MAP_LAMBDA;
     const bool incl = d.diag == SMAP_DIAG_INCLUSIVE;
     if (flags & ~(SMAP_RUN_CHECKSUM | SMAP_RUN_CHECKSUM_MIX | SMAP_RUN_XOR)) return fail(SMAP_E_INVALID, "unknown flags 0x%x", flags);
     if (ipl == PL_EDM && (d.m != 2 || incl)) return fail(SMAP_E_INVALID, "EDM is defined on the m=2 strict domain");
@@ -409,9 +419,6 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, size_t
     if (!tile && reduces && (rm % 32) != 0)
         return fail(SMAP_E_INVALID, "reductions need rho^m to be a multiple of 32 (rho^m = %llu)", (unsigned long long)rm);
 
-    cudaStream_t s = (cudaStream_t)stream;
-    DevGuard guard;                           // the plan's device for this call; restored on every return
-    CK(guard.enter(p->device));
     const bool tc_bits = ipl == PL_TC && tile;
     const int64_t npad = (int64_t)p->P.N * d.rho;          // bitmap over the grid's index range
     if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)npad * (size_t)((npad + 31) / 32) * sizeof(uint32_t)));
@@ -425,37 +432,61 @@ smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, size_t
             p->npartials = np;
         }
     }
-    Params P = p->P;
-    P.pts = points;
-    P.param = param;
-    P.out = out;
-    P.partials = p->d_partials;
-    P.adj = p->d_adj;
+    a->ipl = ipl; a->cs = cs; a->tile = tile; a->incl = incl; a->atm = atm; a->tc_bits = tc_bits; a->npad = npad;
+    a->P = p->P;
+    a->P.pts = points;
+    a->P.param = param;
+    a->P.out = out;
+    a->P.partials = p->d_partials;
+    a->P.adj = p->d_adj;
+    return SMAP_OK;
+}
+
+// Queue the run's kernels on s (plus the CUDA events of smap_stats' kernel_ms when timed).
+static smap_status run_launch(smap_plan_t p, const RunArgs &a, cudaStream_t s, bool timed)
+{
+    const smap_plan_desc &d = p->d;
     uint32_t launches = 0;
-    if (!tc_bits) CK(cudaMemsetAsync(p->d_res, 0, sizeof(Result), s));   // (the TC pre-pass zeroes it itself)
-    CK(cudaEventRecord(p->ev0, s));
+    if (!a.tc_bits) CK(cudaMemsetAsync(p->d_res, 0, sizeof(Result), s));   // (the TC pre-pass zeroes it itself)
+    if (timed) CK(cudaEventRecord(p->ev0, s));
     cudaError_t e;
-    if (tc_bits) {
-        cudaError_t ea = launch_tc_adjacency(points, (int)d.n, (int)npad, param, p->d_adj, p->d_res, s);
+    if (a.tc_bits) {
+        cudaError_t ea = launch_tc_adjacency(a.P.pts, (int)d.n, (int)a.npad, a.P.param, p->d_adj, p->d_res, s);
         if (ea != cudaSuccess) return cuda_fail(ea, "TC adjacency launch");
         launches++;
     }
-    if (!tile) e = d.m == 2 ? launch_thread2(P, d.map, incl, ipl, cs, s) : launch_thread3(P, d.map, ipl, cs, s);
-    else e = d.m == 2 ? launch_tile2(P, d.rho, d.map, incl, ipl, cs, p->ctas, s)
-                      : launch_tile3(P, d.rho, d.map, ipl, cs, p->ctas, s);
+    if (!a.tile) e = d.m == 2 ? launch_thread2(a.P, d.map, a.incl, a.ipl, a.cs, s) : launch_thread3(a.P, d.map, a.ipl, a.cs, s);
+    else e = d.m == 2 ? launch_tile2(a.P, d.rho, d.map, a.incl, a.ipl, a.cs, p->ctas, s)
+                      : launch_tile3(a.P, d.rho, d.map, a.ipl, a.cs, p->ctas, s);
     if (e == cudaErrorInvalidValue) return fail(SMAP_E_UNSUPPORTED, "no kernel for this plan/payload combination");
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     launches++;
-    if (atm) {
-        const uint64_t np = tile ? p->ctas : p->P.nblocks;
+    if (a.atm) {
+        const uint64_t np = a.tile ? p->ctas : p->P.nblocks;
         e = launch_finalize(p->d_partials, np, p->d_scratch, p->d_res, s, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "finalize launch");
     }
-    CK(cudaEventRecord(p->ev1, s));
+    if (timed) CK(cudaEventRecord(p->ev1, s));
     p->last_stream = s;
     p->last_launches = launches;
-    p->ran = 1;
+    p->ran = timed ? 1 : p->ran;
     return SMAP_OK;
+}
+
+extern "C" {
+
+smap_status smap_run(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
+                     void *out, size_t out_bytes, uint32_t flags, void *stream)
+{
+    g_err.clear();
+    if (!p) return fail(SMAP_E_INVALID, "smap_run: NULL plan");
+    if (p->device == SMAP_DEVICE_NONE) return fail(SMAP_E_INVALID, "smap_run on a host-only plan");
+    DevGuard guard;                           // the plan's device for this call; restored on every return
+    CK(guard.enter(p->device));
+    RunArgs a;
+    smap_status st = run_prepare(p, pl, points, points_bytes, param, out, out_bytes, flags, &a);
+    if (st != SMAP_OK) return st;
+    return run_launch(p, a, (cudaStream_t)stream, true);
 }
 
 static void fill_stats(smap_plan_t p, const Result *r, smap_stats *st)
@@ -763,6 +794,74 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p->ev0, p->ev1) == cudaSuccess) stats->kernel_ms = ms;
     return SMAP_OK;
+}
+
+struct smap_graph_s {
+    smap_plan_t p = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint32_t launches = 0;
+};
+
+smap_status smap_graph_capture(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
+                               void *out, size_t out_bytes, uint32_t flags, void *record, smap_graph_t *g)
+{
+    g_err.clear();
+    if (!g) return fail(SMAP_E_INVALID, "smap_graph_capture: NULL graph handle");
+    *g = nullptr;
+    if (!p) return fail(SMAP_E_INVALID, "smap_graph_capture: NULL plan");
+    if (p->device == SMAP_DEVICE_NONE) return fail(SMAP_E_INVALID, "smap_graph_capture on a host-only plan");
+    if ((reinterpret_cast<uintptr_t>(record) & 7) != 0) return fail(SMAP_E_INVALID, "record not 8-byte aligned");
+    DevGuard guard;
+    CK(guard.enter(p->device));
+    RunArgs a;
+    smap_status st = run_prepare(p, pl, points, points_bytes, param, out, out_bytes, flags, &a);   // (allocates outside the capture)
+    if (st != SMAP_OK) return st;
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) { cudaStreamDestroy(cs); return cuda_fail(e, "cudaStreamBeginCapture"); }
+    st = run_launch(p, a, cs, false);
+    uint32_t launches = p->last_launches;
+    if (st == SMAP_OK && record) {
+        e = launch_result_reduce(p->d_res, reinterpret_cast<smap_result *>(record), cs);
+        if (e != cudaSuccess) st = cuda_fail(e, "result reduce launch");
+        launches++;
+    }
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    if (st != SMAP_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+    if (e != cudaSuccess) { if (graph) cudaGraphDestroy(graph); return cuda_fail(e, "cudaStreamEndCapture"); }
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e != cudaSuccess) { cudaGraphDestroy(graph); return cuda_fail(e, "cudaGraphInstantiate"); }
+    smap_graph_s *h = new (std::nothrow) smap_graph_s();
+    if (!h) { cudaGraphExecDestroy(exec); cudaGraphDestroy(graph); return fail(SMAP_E_NOMEM, "host allocation failed"); }
+    h->p = p; h->graph = graph; h->exec = exec; h->launches = launches;
+    *g = h;
+    return SMAP_OK;
+}
+
+smap_status smap_graph_launch(smap_graph_t g, void *stream)
+{
+    if (!g || !g->exec) return fail(SMAP_E_INVALID, "smap_graph_launch: NULL graph");
+    DevGuard guard;
+    CK(guard.enter(g->p->device));
+    CK(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+    return SMAP_OK;
+}
+
+uint32_t smap_graph_launches(smap_graph_t g) { return g ? g->launches : 0; }
+
+void smap_graph_destroy(smap_graph_t g)
+{
+    if (!g) return;
+    DevGuard guard;
+    if (g->p && g->p->device >= 0) guard.enter(g->p->device);
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
 }
 
 void smap_destroy(smap_plan_t p)

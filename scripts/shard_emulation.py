@@ -1,14 +1,17 @@
 """Per-rank device time of the sharded launches, emulated on ONE GPU: every
-rank r of G runs its omega_x column shard back to back;
-the max over ranks is the kernel time a G-GPU run would see per step (the
-collective -- one all-gather of 56 bytes -- comes on top).  Writes
-gpurun_out/shards.json.
+rank r of G runs its omega_x column shard as bench.py's
+configs_sharded does -- one CUDA graph per rank step (payload kernels + the
+record reduction, smap_graph_capture) -- and the max over ranks is the step
+time a G-GPU run would see (the collective, one all-gather of 56 bytes, comes
+on top).  Ranks are timed interleaved, in both orders, so that clock and
+power drift hit every rank alike.  Writes gpurun_out/shards.json.
 
-    python scripts/shard_emulation.py
+    python scripts/shard_emulation.py [--only C5,C5X] [--reps 9]
 """
+import argparse
 import json
-import math
 import os
+import statistics
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -18,45 +21,58 @@ import torch
 import paper_1610_07394_b200 as sm
 import workloads
 
-
-def med(plan, payload, pts=None, param=0.0, out=None, flags=0, reps=8):
-    for _ in range(2):
-        sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
-    for a, b in ev:
-        a.record()
-        sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags)
-        b.record()
-    torch.cuda.synchronize()
-    ts = sorted(a.elapsed_time(b) for a, b in ev)
-    return ts[len(ts) // 2]
+CASES = {"C2": (2, "edm", workloads.SEED_C2, 0.0), "C3": (3, "index_write_atm", workloads.SEED_C3, 1e-2),
+         "C4": (2, "index_write", None, 0.0), "C5": (3, "tc", workloads.SEED_C5, 0.5),
+         "C5X": (3, "tc", workloads.SEED_C5X, 0.5)}
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="C2,C3,C4,C5,C5X")
+    ap.add_argument("--reps", type=int, default=9)
+    ap.add_argument("--gs", default="1,2,4,8")
+    a = ap.parse_args()
     rows = []
-    cases = [("C2 EDM", 2, workloads.CONFIGS["C2"]["n"], "edm", workloads.BENCH_EDM, workloads.SEED_C2, 0.0, sm.RUN_XOR),
-             ("C3 IW+ATM", 3, workloads.CONFIGS["C3"]["n"], "index_write_atm", workloads.BENCH_C3, workloads.SEED_C3, 1e-2,
-              sm.RUN_XOR),
-             ("C4 IW u64", 2, workloads.CONFIGS["C4"]["n"], "index_write", workloads.BENCH_C4, None, 0.0, sm.RUN_XOR),
-             ("C5 TC", 3, workloads.CONFIGS["C5"]["n"], "tc", workloads.BENCH_C5, workloads.SEED_C5, 0.5, 0)]
-    for name, m, n, payload, cfg, seed, param, flags in cases:
+    for name in a.only.split(","):
+        m, payload, seed, param = CASES[name]
+        n = workloads.C5X["n"] if name == "C5X" else workloads.CONFIGS[name]["n"]
         pts = torch.from_numpy(workloads.points(n, seed)).cuda() if seed else None
-        row = {"config": name, "launch": cfg, "ranks": {}}
-        for G in (1, 2, 4, 8):
-            times = []
+        flags = sm.RUN_XOR if payload in ("edm", "index_write") else 0
+        row = {"config": name, "n": n, "payload": payload, "ranks": {}}
+        for G in (int(g) for g in a.gs.split(",")):
+            launch = workloads.sharded_launch(name, G)
+            ranks = []
             for r in range(G):
-                plan = sm.smap_plan(m, n, shard_rank=r, shard_count=G, **cfg)
+                plan = sm.smap_plan(m, n, shard_rank=r, shard_count=G, **launch)
                 out = sm.alloc_out(plan, payload)
-                times.append(med(plan, payload, pts, param, out, flags))
-                st = sm.smap_stats_fetch(plan)
-                del out
+                rec = torch.zeros(7, dtype=torch.int64, device="cuda")
+                g = sm.smap_graph_capture(plan, payload, points=pts, param=param, out=out, flags=flags, record=rec)
+                ranks.append((plan, out, rec, g))
+                if name == "C4" and G == 1:
+                    break
+            times = [[] for _ in ranks]
+            for rep in range(a.reps + 2):
+                order = list(range(len(ranks))) if rep % 2 == 0 else list(reversed(range(len(ranks))))
+                for r in order:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    sm.smap_graph_launch(ranks[r][3])
+                    e1.record()
+                    torch.cuda.synchronize()
+                    if rep >= 2:
+                        times[r].append(e0.elapsed_time(e1))
+            med = [statistics.median(t) for t in times]
+            tot = {k: sum(sm.result_dict(x[2])[k] for x in ranks) for k in ("count", "tc")}
+            row["ranks"][G] = {"launch": launch, "max_ms": round(max(med), 4), "min_ms": round(min(med), 4),
+                               "per_rank_ms": [round(x, 4) for x in med], "count": tot["count"], "tc": tot["tc"]}
+            del ranks
             torch.cuda.empty_cache()
-            row["ranks"][G] = {"max_ms": round(max(times), 4), "min_ms": round(min(times), 4),
-                               "speedup_vs_1": None}
-        t1 = row["ranks"][1]["max_ms"]
-        for G in (1, 2, 4, 8):
+        t1 = row["ranks"][min(row["ranks"])]["max_ms"]
+        for G in row["ranks"]:
             row["ranks"][G]["speedup_vs_1"] = round(t1 / row["ranks"][G]["max_ms"], 3)
-        print(json.dumps(row), flush=True)
+            row["ranks"][G]["max_over_min"] = round(row["ranks"][G]["max_ms"] / row["ranks"][G]["min_ms"], 3)
+        print(json.dumps({"config": name, **{G: (v["max_ms"], v["speedup_vs_1"], v["max_over_min"])
+                                              for G, v in row["ranks"].items()}}), flush=True)
         rows.append(row)
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/shards.json", "w") as f:

@@ -1,0 +1,83 @@
+"""smap_graph_capture / smap_graph_launch (include/smap.h): a captured step
+replays the same kernels as smap_run + smap_result_reduce, so its device
+record must equal the direct run's, bit for bit, on every replay; the bound
+output buffer must hold the same values.  Checked against the oracle where
+the payload has a cheap oracle value."""
+import math
+
+import numpy as np
+import pytest
+
+import workloads
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sm():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1610_07394_b200 as s
+    return s
+
+
+CASES = [
+    (2, 2048, dict(rho=128, granularity="tile", layout="tiles"), "edm", 0.0, "xor"),
+    (2, 4096, dict(rho=128, granularity="tile", layout="tiles"), "index_write", 0.0, "checksum"),
+    (3, 512, dict(rho=32, granularity="tile", layout="tiles"), "index_write_atm", 1e-2, "none"),
+    (3, 512, dict(rho=32, granularity="tile"), "atm", 1e-2, "none"),
+    (3, 1024, dict(rho=64, granularity="tile", persistent=8), "tc", 0.5, "none"),
+    (3, 256, dict(rho=8, granularity="thread"), "tc", 0.5, "none"),
+    (2, 1024, dict(rho=16, granularity="thread"), "edm", 0.0, "mix"),
+]
+
+
+@pytest.mark.parametrize("m,n,kw,payload,param,mode", CASES)
+def test_graph_replay_equals_direct_run(sm, orc, m, n, kw, payload, param, mode):
+    flags = {"none": 0, "xor": sm.RUN_XOR, "checksum": sm.RUN_CHECKSUM, "mix": sm.RUN_CHECKSUM_MIX}[mode]
+    plan = sm.smap_plan(m, n, **kw)
+    p = workloads.points(n, 11)
+    pts = torch.from_numpy(p).cuda() if payload in ("edm", "atm", "tc", "index_write_atm") else None
+    out = sm.alloc_out(plan, payload)
+    rec_direct = torch.zeros(7, dtype=torch.int64, device="cuda")
+    sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags)
+    sm.smap_result_reduce(plan, rec_direct)
+    direct = sm.result_dict(rec_direct)
+    ref_out = out.clone() if out is not None else None
+    rec = torch.zeros(7, dtype=torch.int64, device="cuda")
+    g = sm.smap_graph_capture(plan, payload, points=pts, param=param, out=out, flags=flags, record=rec)
+    assert g.launches >= 2                                      # the payload kernel(s) + the reduction
+    if out is not None:
+        out.zero_()
+    for _ in range(3):
+        sm.smap_graph_launch(g)
+        torch.cuda.synchronize()
+        assert sm.result_dict(rec) == direct
+    if out is not None:
+        assert torch.equal(out, ref_out)
+    V = sm.smap_volume(m, n)
+    assert direct["count"] == V
+    if payload == "tc":
+        assert direct["tc"] == orc.tc_count(p, np.float32(param))
+    if payload in ("atm", "index_write_atm"):
+        ref = orc.atm_sum(p, np.float32(param))
+        assert abs(direct["sum"] - ref) <= 1e-5 * abs(ref)
+    if payload == "edm" and flags == sm.RUN_XOR:
+        assert direct["xr"] == orc.cs_edm(p)["xr"]
+
+
+def test_graph_capture_validates(sm):
+    plan = sm.smap_plan(2, 1024, 128, granularity="tile", layout="tiles")
+    out = sm.alloc_out(plan, "edm")
+    with pytest.raises(sm.SmapError):                          # EDM without points: rejected before capture
+        sm.smap_graph_capture(plan, "edm", out=out)
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    with pytest.raises(sm.SmapError):                          # misaligned record
+        sm.smap_graph_capture(plan, "index_write", out=out.view(torch.int32), record=rec.data_ptr() + 4)
+    # a stream-ordered replay on a side stream is ordered with the work on that stream
+    g = sm.smap_graph_capture(plan, "index_write", out=out.view(torch.int32), flags=sm.RUN_XOR, record=rec)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        sm.smap_graph_launch(g, stream=s)
+    s.synchronize()
+    assert sm.result_dict(rec)["count"] == math.comb(1024, 2)
