@@ -119,6 +119,12 @@ typedef enum {
 #define SMAP_RUN_CHECKSUM     0x1u /* INDEX_WRITE(_ATM)/EDM: accumulate s0, s1 (E21) */
 #define SMAP_RUN_CHECKSUM_MIX 0x2u /* INDEX_WRITE(_ATM)/EDM: also accumulate mix (E21); implies CHECKSUM */
 #define SMAP_RUN_XOR          0x4u /* INDEX_WRITE(_ATM)/EDM: count and xr only (the cheapest fused reduction, E21) */
+#define SMAP_RUN_FAST_SQRT    0x8u /* EDM only: on the full tiles of a TILE rho >= 128 tile-blocked (E23) plan, the
+                                    * distance is sqrt.approx.ftz (one MUFU.SQRT, relative error < 2^-22 -- inside the
+                                    * north star's 1e-5, NOT bit-identical to the correctly rounded sqrt of E17);
+                                    * every other tile, and any warp whose points include a nonzero coordinate below
+                                    * 2^-40 in magnitude, keeps the exact path.  Fewer SM instructions per pair: for
+                                    * the power-capped (sustained) regime. */
 
 typedef struct smap_plan_s *smap_plan_t;
 

@@ -34,6 +34,7 @@ DEVICE_NONE = -2          # smap_plan(device=DEVICE_NONE): host-only plan (valid
 RUN_CHECKSUM = 0x1
 RUN_CHECKSUM_MIX = 0x2
 RUN_XOR = 0x4
+RUN_FAST_SQRT = 0x8      # EDM: sqrt.approx on the vector tile path (1e-5, not bit-exact)
 
 
 class SmapError(RuntimeError):
@@ -407,4 +408,5 @@ def alloc_out(plan: Plan, payload: str, device="cuda", zero: bool = False):
 __all__ = ["smap_plan", "smap_plan_query", "smap_out_bytes", "smap_run", "smap_run_host", "smap_stats_fetch",
            "smap_result_reduce", "smap_result_combine", "smap_graph_capture", "smap_graph_launch", "Graph",
            "smap_volume", "smap_destroy", "smap_last_error", "smap_abi_version", "Plan", "SmapError",
-           "alloc_out", "exported_symbols", "RUN_CHECKSUM", "RUN_CHECKSUM_MIX", "RUN_XOR"]
+           "alloc_out", "exported_symbols", "RUN_CHECKSUM", "RUN_CHECKSUM_MIX", "RUN_XOR",
+           "RUN_FAST_SQRT"]

@@ -382,7 +382,9 @@ static smap_status run_prepare(smap_plan_t p, smap_payload pl, const float *poin
     const smap_plan_desc &d = p->d;
     const bool tile = d.granularity == SMAP_GRAN_TILE;
     const bool incl = d.diag == SMAP_DIAG_INCLUSIVE;
-    if (flags & ~(SMAP_RUN_CHECKSUM | SMAP_RUN_CHECKSUM_MIX | SMAP_RUN_XOR)) return fail(SMAP_E_INVALID, "unknown flags 0x%x", flags);
+    if (flags & ~(SMAP_RUN_CHECKSUM | SMAP_RUN_CHECKSUM_MIX | SMAP_RUN_XOR | SMAP_RUN_FAST_SQRT))
+        return fail(SMAP_E_INVALID, "unknown flags 0x%x", flags);
+    if ((flags & SMAP_RUN_FAST_SQRT) && ipl != PL_EDM) return fail(SMAP_E_INVALID, "SMAP_RUN_FAST_SQRT is an EDM flag");
     if (ipl == PL_EDM && (d.m != 2 || incl)) return fail(SMAP_E_INVALID, "EDM is defined on the m=2 strict domain");
     const bool atm = pl_atm(ipl);
     if ((atm || ipl == PL_TC) && d.m != 3) return fail(SMAP_E_INVALID, "ATM/TC are m=3 payloads");
@@ -436,6 +438,7 @@ static smap_status run_prepare(smap_plan_t p, smap_payload pl, const float *poin
     a->P = p->P;
     a->P.pts = points;
     a->P.param = param;
+    a->P.fsqrt = (flags & SMAP_RUN_FAST_SQRT) ? 1 : 0;
     a->P.out = out;
     a->P.partials = p->d_partials;
     a->P.adj = p->d_adj;

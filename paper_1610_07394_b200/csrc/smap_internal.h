@@ -63,6 +63,7 @@ struct Params {
     const uint32_t *adj;           // TC (TILE): pair-predicate bitmap, n rows of n/32 words
     const Piece *pieces;           // SMAP_MAP_BELOW: the decomposition, sorted by start
     int npieces;
+    int fsqrt;                     // EDM (SMAP_RUN_FAST_SQRT): sqrt.approx on the vector tile path
 };
 
 // ---------------------------------------------------------------- m=3 tile-blocked layout (E26)

@@ -81,3 +81,52 @@ def test_edm_vs_fp64_definition(sm, orc, kw, pts):
     rel = np.abs(got[~zero] - ref[~zero]) / ref[~zero]
     assert rel.max() <= 1e-5, rel.max()
     assert rel.max() <= 1e-6, rel.max()
+
+
+FAST_KW = [dict(rho=256, granularity="tile", map="lambda", layout="tiles"),
+           dict(rho=128, granularity="tile", map="lambda", layout="tiles"),
+           dict(rho=256, granularity="tile", map="bb", layout="tiles")]
+
+
+@pytest.mark.parametrize("kw", FAST_KW, ids=lambda k: "-".join(str(v) for v in k.values()))
+@pytest.mark.parametrize("pts", ["uniform", "duplicates", "clustered_scale", "tiny"])
+def test_edm_fast_sqrt_vs_fp64_definition(sm, orc, kw, pts):
+    """SMAP_RUN_FAST_SQRT (sqrt.approx on the vector tile path): every distance within the
+    north_star's 1e-5 of the fp64 definition; zero distances exact; a point set with
+    coordinates below 2^-40 takes the exact path (bit-identical to the default run)."""
+    n = 2048
+    if pts == "uniform":
+        p = workloads.points(n, workloads.SEED_C2)
+    elif pts == "duplicates":
+        p = workloads.clustered_points(n, 5)
+    elif pts == "clustered_scale":
+        p = (np.float32(1000.0) + workloads.points(n, 12) * np.float32(1e-2)).astype(np.float32)
+    else:
+        # coordinates ~1e-15 (below the 2^-40 staging bound, so every warp must take the
+        # exact path) whose squared distances ~1e-30 are still normal fp32 numbers
+        p = (workloads.points(n, 13) * np.float32(1e-15)).astype(np.float32)
+    plan = sm.smap_plan(2, n, **kw)
+    pt = torch.from_numpy(p).cuda()
+    fast = sm.alloc_out(plan, "edm")
+    exact = sm.alloc_out(plan, "edm")
+    sm.smap_run(plan, "edm", points=pt, out=fast, flags=sm.RUN_XOR | sm.RUN_FAST_SQRT)
+    assert sm.smap_stats_fetch(plan)["count"] == sm.smap_volume(2, n)
+    sm.smap_run(plan, "edm", points=pt, out=exact, flags=sm.RUN_XOR)
+    got = canonical(sm, orc, kw, fast, n).astype(np.float64)
+    ref = edm_fp64(p)
+    zero = ref == 0.0
+    assert (got[zero] == 0.0).all()
+    rel = np.abs(got[~zero] - ref[~zero]) / ref[~zero]
+    assert rel.max() <= 1e-5, rel.max()
+    same = torch.equal(fast, exact)
+    if pts == "tiny":
+        assert same                                            # the staging check sent every warp to the exact path
+    elif pts == "uniform":
+        assert not same                                        # the approximate path ran (it rounds differently somewhere)
+
+
+def test_fast_sqrt_flag_is_edm_only(sm):
+    plan = sm.smap_plan(2, 1024, 128, granularity="tile", layout="tiles")
+    out = sm.alloc_out(plan, "index_write")
+    with pytest.raises(sm.SmapError):
+        sm.smap_run(plan, "index_write", out=out, flags=sm.RUN_FAST_SQRT)
