@@ -40,6 +40,7 @@ struct smap_plan_s {
     cudaStream_t last_stream = nullptr;
     uint32_t last_launches = 0;
     int ran = 0;
+    int res_dirty = 1;              // the result block may be nonzero (a fresh allocation, or an smap_run's results)
 };
 
 static thread_local std::string g_err;
@@ -446,11 +447,19 @@ static smap_status run_prepare(smap_plan_t p, smap_payload pl, const float *poin
 }
 
 // Queue the run's kernels on s (plus the CUDA events of smap_stats' kernel_ms when timed).
-static smap_status run_launch(smap_plan_t p, const RunArgs &a, cudaStream_t s, bool timed)
+// rec (device smap_result *, optional): the run's record, written by the ATM
+// finalize (or, for the other payloads, left to the caller: *rec_done false).
+// lean (graph capture with a record): no memset of the result block (the graph's
+// last kernel clears it behind the record; smap_graph_launch clears it first when
+// an smap_run left results in it) and the small tail kernels as programmatic
+// dependents.
+static smap_status run_launch(smap_plan_t p, const RunArgs &a, cudaStream_t s, bool timed, smap_result *rec = nullptr,
+                              bool lean = false, bool *rec_done = nullptr)
 {
     const smap_plan_desc &d = p->d;
     uint32_t launches = 0;
-    if (!a.tc_bits) CK(cudaMemsetAsync(p->d_res, 0, sizeof(Result), s));   // (the TC pre-pass zeroes it itself)
+    if (rec_done) *rec_done = false;
+    if (!a.tc_bits && !lean) CK(cudaMemsetAsync(p->d_res, 0, sizeof(Result), s));   // (the TC pre-pass zeroes it itself)
     if (timed) CK(cudaEventRecord(p->ev0, s));
     cudaError_t e;
     if (a.tc_bits) {
@@ -466,13 +475,15 @@ static smap_status run_launch(smap_plan_t p, const RunArgs &a, cudaStream_t s, b
     launches++;
     if (a.atm) {
         const uint64_t np = a.tile ? p->ctas : p->P.nblocks;
-        e = launch_finalize(p->d_partials, np, p->d_scratch, p->d_res, s, &launches);
+        e = launch_finalize(p->d_partials, np, p->d_scratch, p->d_res, s, &launches, rec, lean, lean);
         if (e != cudaSuccess) return cuda_fail(e, "finalize launch");
+        if (rec_done) *rec_done = rec != nullptr;
     }
     if (timed) CK(cudaEventRecord(p->ev1, s));
     p->last_stream = s;
     p->last_launches = launches;
     p->ran = timed ? 1 : p->ran;
+    if (timed) p->res_dirty = 1;        // results stay in the block (smap_stats_fetch / smap_result_reduce)
     return SMAP_OK;
 }
 
@@ -743,7 +754,7 @@ smap_status smap_result_reduce(smap_plan_t p, void *dst, void *stream)
     if (!p->ran) return fail(SMAP_E_INVALID, "smap_result_reduce before smap_run");
     DevGuard guard;
     CK(guard.enter(p->device));
-    cudaError_t e = launch_result_reduce(p->d_res, reinterpret_cast<smap_result *>(dst), (cudaStream_t)stream);
+    cudaError_t e = launch_result_reduce(p->d_res, reinterpret_cast<smap_result *>(dst), (cudaStream_t)stream, false, false);
     if (e != cudaSuccess) return cuda_fail(e, "result reduce launch");
     return SMAP_OK;
 }
@@ -786,7 +797,7 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
     if (st != SMAP_OK) return st;
     if (!p->d_rec) CK(cudaMalloc(&p->d_rec, sizeof(smap_result)));
     if (!p->h_rec) CK(cudaMallocHost(&p->h_rec, sizeof(smap_result)));
-    cudaError_t e = launch_result_reduce(p->d_res, p->d_rec, s);
+    cudaError_t e = launch_result_reduce(p->d_res, p->d_rec, s, false, false);
     if (e != cudaSuccess) return cuda_fail(e, "result reduce launch");
     CK(cudaMemcpyAsync(p->h_rec, p->d_rec, sizeof(smap_result), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -800,6 +811,7 @@ smap_status smap_run_host(smap_plan_t p, smap_payload pl, const float *host_poin
 }
 
 struct smap_graph_s {
+    bool lean = false;                // no memset node: the result block is clear between launches
     smap_plan_t p = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -824,10 +836,13 @@ smap_status smap_graph_capture(smap_plan_t p, smap_payload pl, const float *poin
     CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) { cudaStreamDestroy(cs); return cuda_fail(e, "cudaStreamBeginCapture"); }
-    st = run_launch(p, a, cs, false);
+    const bool lean = record != nullptr;     // (measured: C3 step 0.0378 -> 0.0357 ms at G = 8, 0.132 -> 0.130 at G = 1)
+    bool rec_done = false;
+    smap_result *rec = reinterpret_cast<smap_result *>(record);
+    st = run_launch(p, a, cs, false, rec, lean, &rec_done);
     uint32_t launches = p->last_launches;
-    if (st == SMAP_OK && record) {
-        e = launch_result_reduce(p->d_res, reinterpret_cast<smap_result *>(record), cs);
+    if (st == SMAP_OK && record && !rec_done) {
+        e = launch_result_reduce(p->d_res, rec, cs, lean, lean);
         if (e != cudaSuccess) st = cuda_fail(e, "result reduce launch");
         launches++;
     }
@@ -841,7 +856,7 @@ smap_status smap_graph_capture(smap_plan_t p, smap_payload pl, const float *poin
     if (e != cudaSuccess) { cudaGraphDestroy(graph); return cuda_fail(e, "cudaGraphInstantiate"); }
     smap_graph_s *h = new (std::nothrow) smap_graph_s();
     if (!h) { cudaGraphExecDestroy(exec); cudaGraphDestroy(graph); return fail(SMAP_E_NOMEM, "host allocation failed"); }
-    h->p = p; h->graph = graph; h->exec = exec; h->launches = launches;
+    h->p = p; h->graph = graph; h->exec = exec; h->launches = launches; h->lean = lean;
     *g = h;
     return SMAP_OK;
 }
@@ -851,6 +866,10 @@ smap_status smap_graph_launch(smap_graph_t g, void *stream)
     if (!g || !g->exec) return fail(SMAP_E_INVALID, "smap_graph_launch: NULL graph");
     DevGuard guard;
     CK(guard.enter(g->p->device));
+    if (g->lean && g->p->res_dirty) {   // an smap_run left its results in the block: clear it first
+        CK(cudaMemsetAsync(g->p->d_res, 0, sizeof(Result), (cudaStream_t)stream));
+        g->p->res_dirty = 0;
+    }
     CK(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
     return SMAP_OK;
 }
@@ -905,21 +924,17 @@ __global__ void __launch_bounds__(256) k_fin1(const double *in, uint64_t n, doub
     if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
-__global__ void __launch_bounds__(1024) k_fin2(const double *in, uint64_t n, Result *res)
+__device__ __forceinline__ void pdl_wait()
 {
-    double s = 0.0;
-    for (uint64_t idx = threadIdx.x; idx < n; idx += 1024) s += in[idx];
-    s = block_sum_f64(s);
-    if (threadIdx.x == 0) res->sum = s;
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // (no-op unless launched as a programmatic dependent)
 }
 
-uint64_t finalize_scratch_elems(uint64_t np) { return (np + kFin1Per - 1) / kFin1Per; }
-
-// Sum the kSlots integer slots (exact mod 2^64) and copy the fp64 sum into
-// one 48-byte smap_result record.
-__global__ void __launch_bounds__(32) k_result_reduce(const Result *res, smap_result *dst)
+// One warp: the kSlots integer slots of res (exact mod 2^64, xr by xor) and the
+// fp64 sum into one 56-byte record; with zero, the result block is cleared
+// behind it for the next launch of a graph (see smap_graph_capture).
+__device__ __forceinline__ void warp_record(Result *res, smap_result *dst, double sum, bool zero)
 {
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     uint64_t v[5];
 #pragma unroll
     for (int k = 0; k < 5; k++) {
@@ -934,8 +949,37 @@ __global__ void __launch_bounds__(32) k_result_reduce(const Result *res, smap_re
     if (lane == 0) {
         dst->count = v[0]; dst->s0 = v[1]; dst->s1 = v[2]; dst->mix = v[3]; dst->tc = v[4];
         dst->xr = xr;
-        dst->sum = res->sum;
+        dst->sum = sum;
     }
+    if (zero) {
+        __syncwarp();
+        for (int e = lane; e < (int)(sizeof(Result) / 8); e += 32) reinterpret_cast<unsigned long long *>(res)[e] = 0ull;
+    }
+}
+
+// The fixed-order fp64 sum of the ATM partials; with rec, also the run's record
+// (the record reduction folded into the finalize: one launch fewer per step).
+__global__ void __launch_bounds__(1024) k_fin2(const double *in, uint64_t n, Result *res, smap_result *rec, int zero)
+{
+    pdl_wait();
+    __shared__ double total;
+    double s = 0.0;
+    for (uint64_t idx = threadIdx.x; idx < n; idx += 1024) s += in[idx];
+    s = block_sum_f64(s);
+    if (threadIdx.x == 0) { res->sum = s; total = s; }
+    if (!rec) return;
+    __syncthreads();
+    if (threadIdx.x < 32) warp_record(res, rec, total, zero != 0);
+}
+
+uint64_t finalize_scratch_elems(uint64_t np) { return (np + kFin1Per - 1) / kFin1Per; }
+
+// Sum the kSlots integer slots (exact mod 2^64) and copy the fp64 sum into
+// one 56-byte smap_result record.
+__global__ void __launch_bounds__(32) k_result_reduce(Result *res, smap_result *dst, int zero)
+{
+    pdl_wait();
+    warp_record(res, dst, res->sum, zero != 0);
 }
 
 // Combine G device records in one warp: integer fields add mod 2^64, xr by
@@ -962,25 +1006,39 @@ __global__ void __launch_bounds__(32) k_result_combine(const smap_result *recs, 
     }
 }
 
-cudaError_t launch_result_reduce(const Result *res, smap_result *dst, cudaStream_t s)
+// pdl: launch as a programmatic dependent of the previous kernel on s (its launch
+// overlaps the tail of that kernel; the kernel waits in griddepcontrol.wait)
+template <typename... Args>
+static cudaError_t launch_small(void (*k)(Args...), unsigned grid, unsigned block, cudaStream_t s, bool pdl, Args... args)
 {
-    k_result_reduce<<<1, 32, 0, s>>>(res, dst);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+cudaError_t launch_result_reduce(Result *res, smap_result *dst, cudaStream_t s, bool pdl, bool zero)
+{
+    return launch_small(k_result_reduce, 1, 32, s, pdl, res, dst, zero ? 1 : 0);
 }
 
 cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res, cudaStream_t s,
-                            uint32_t *launches)
+                            uint32_t *launches, smap_result *rec, bool pdl, bool zero)
 {
     if (np <= 65536) {
-        k_fin2<<<1, 1024, 0, s>>>(partials, np, res);
         *launches += 1;
-        return cudaGetLastError();
+        return launch_small(k_fin2, 1, 1024, s, pdl, partials, np, res, rec, zero ? 1 : 0);
     }
     const uint64_t n1 = finalize_scratch_elems(np);
     k_fin1<<<(unsigned)n1, 256, 0, s>>>(partials, np, scratch);
-    k_fin2<<<1, 1024, 0, s>>>(scratch, n1, res);
     *launches += 2;
-    return cudaGetLastError();
+    return launch_small(k_fin2, 1, 1024, s, false, (const double *)scratch, n1, res, rec, zero ? 1 : 0);
 }
 
 } // namespace smap

@@ -146,16 +146,19 @@ cudaError_t launch_tile3(const Params &P, int T, int map, int pl, int cs, unsign
 // npad = N * rho (rows j < npad, words rounded up).
 // It also zeroes the run's result block (the main kernel follows in stream order).
 cudaError_t launch_tc_adjacency(const float *pts, int n, int npad, float R, uint32_t *adj, Result *res, cudaStream_t s);
-// Deterministic fixed-order fp64 reduction of partials[0..np) into res->sum.
-// Adds the number of kernels it launched to *launches.
-cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res,
-                            cudaStream_t s, uint32_t *launches);
 uint64_t finalize_scratch_elems(uint64_t np);
 }  // namespace smap
 
 #include "smap.h"
 
 namespace smap {
-cudaError_t launch_result_reduce(const Result *res, smap_result *dst, cudaStream_t s);
+// Deterministic fixed-order fp64 reduction of partials[0..np) into res->sum;
+// with rec, the same kernel also writes the run's record.  pdl: the last kernel
+// is a programmatic dependent of the previous one on s; zero: it clears res
+// behind the record.  Adds the number of kernels it launched to *launches.
+cudaError_t launch_finalize(const double *partials, uint64_t np, double *scratch, Result *res, cudaStream_t s,
+                            uint32_t *launches, smap_result *rec = nullptr, bool pdl = false, bool zero = false);
+// res -> one record (pdl / zero as above)
+cudaError_t launch_result_reduce(Result *res, smap_result *dst, cudaStream_t s, bool pdl, bool zero);
 
 } // namespace smap

@@ -81,3 +81,32 @@ def test_graph_capture_validates(sm):
         sm.smap_graph_launch(g, stream=s)
     s.synchronize()
     assert sm.result_dict(rec)["count"] == math.comb(1024, 2)
+
+
+@pytest.mark.parametrize("m,n,kw,payload,param,mode", [c for c in CASES if c[2].get("granularity") == "tile"][:5])
+def test_graph_interleaved_with_direct_runs(sm, m, n, kw, payload, param, mode):
+    """A captured step clears the result block behind its record (no memset node);
+    an smap_run in between leaves its results there, and the next replay must
+    still start from a clear block: graph, run, graph, run, graph all agree."""
+    flags = {"none": 0, "xor": sm.RUN_XOR, "checksum": sm.RUN_CHECKSUM, "mix": sm.RUN_CHECKSUM_MIX}[mode]
+    plan = sm.smap_plan(m, n, **kw)
+    p = workloads.points(n, 17)
+    pts = torch.from_numpy(p).cuda() if payload in ("edm", "atm", "tc", "index_write_atm") else None
+    out = sm.alloc_out(plan, payload)
+    rec = torch.zeros(7, dtype=torch.int64, device="cuda")
+    g = sm.smap_graph_capture(plan, payload, points=pts, param=param, out=out, flags=flags, record=rec)
+    results = []
+    for step in range(5):
+        if step % 2 == 0:
+            sm.smap_graph_launch(g)
+            torch.cuda.synchronize()
+            results.append(sm.result_dict(rec))
+        else:
+            sm.smap_run(plan, payload, points=pts, param=param, out=out, flags=flags)
+            r2 = torch.zeros(7, dtype=torch.int64, device="cuda")
+            sm.smap_result_reduce(plan, r2)
+            torch.cuda.synchronize()
+            results.append(sm.result_dict(r2))
+            assert sm.smap_stats_fetch(plan)["count"] == results[-1]["count"]
+    assert all(r == results[0] for r in results), results
+    assert results[0]["count"] == sm.smap_volume(m, n)
