@@ -269,8 +269,13 @@ smap_status smap_result_combine(const void *records, int count, void *dst, void 
  * work between them, which matters for steps of tens of microseconds (C3, C5).  Buffers
  * (points, out, record) and the plan are bound at capture time: they must outlive the
  * graph and not move.  Results of a replay are read from `record` (a device smap_result,
- * 8-byte aligned); smap_stats_fetch / kernel_ms describe the last smap_run only.  Errors as
- * smap_run; SMAP_E_CUDA if the capture or instantiation fails. */
+ * 8-byte aligned); smap_stats_fetch / kernel_ms describe the last smap_run only.  With a
+ * record, the graph has no memset node: its last kernel (the record reduction, folded into
+ * the ATM finalize for ATM payloads, launched as a programmatic dependent) clears the
+ * plan's result block behind the record, and smap_graph_launch clears it first on `stream`
+ * when an smap_run left its results there.  A plan's runs and replays must therefore be
+ * stream-ordered (they share the result block).  Errors as smap_run; SMAP_E_CUDA if the
+ * capture or instantiation fails. */
 typedef struct smap_graph_s *smap_graph_t;
 smap_status smap_graph_capture(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
                                void *out, size_t out_bytes, uint32_t flags, void *record, smap_graph_t *g);
