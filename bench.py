@@ -494,7 +494,8 @@ def config_table(ctx, peak_gbs, f_sm_mhz, reps=10):
     t_iw = med(p1, "index_write", out=out, flags=sm.RUN_XOR)
     t_atm = med(p1, "atm", pts=pts3, param=c3["eps2"])
     gbs = V3 * 4 / (e["lambda_ms"] * 1e-3) / 1e9
-    # E27: 15 FP32 lane operations per triple (14 packed ops + the packed accumulate per two triples)
+    # E27 (round 2 form): 11 FP32 lane operations per triple (11 packed ops, accumulate included, per two
+    # triples); ncu's FMA-pipe % is higher: it also counts table staging and the IMADs of addressing
     fp32_peak = 148 * 128 * f_hz
     e.update(bound="FMA pipe (ATM terms) with the 714 MB index write riding along", atm_sum=st["sum"],
              separate_passes_ms={"index_write": round(t_iw, 4), "atm": round(t_atm, 4)},
@@ -502,9 +503,9 @@ def config_table(ctx, peak_gbs, f_sm_mhz, reps=10):
              overlap_efficiency=round(max(t_iw, t_atm) / e["lambda_ms"], 3),
              index_write_gbs=round(gbs, 1), index_write_frac_of_peak=round(gbs / peak_gbs, 4),
              index_write_alone_gbs=round(V3 * 4 / (t_iw * 1e-3) / 1e9, 1),
-             atm_fp32_pipe_frac=round(V3 * 15 / (t_atm * 1e-3) / fp32_peak, 4),
-             fused_fp32_pipe_frac=round(V3 * 15 / (e["lambda_ms"] * 1e-3) / fp32_peak, 4),
-             pipe_note="FP32-pipe fraction = 15 FP32 lane-ops per triple (E27 term, packed f32x2) x triples / "
+             atm_fp32_pipe_frac=round(V3 * 11 / (t_atm * 1e-3) / fp32_peak, 4),
+             fused_fp32_pipe_frac=round(V3 * 11 / (e["lambda_ms"] * 1e-3) / fp32_peak, 4),
+             pipe_note="FP32-pipe fraction = 11 FP32 lane-ops per triple (E27 term, packed f32x2) x triples / "
                        f"time / (148 SM x 128 lanes x {f_hz / 1e6:.0f} MHz)")
     th, _ = pair(3, n, "index_write_atm", dict(rho=8, granularity="thread"), pts=pts3, param=c3["eps2"], out=out,
                  flags=sm.RUN_XOR, k=max(3, reps // 2))

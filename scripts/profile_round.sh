@@ -17,6 +17,8 @@ $FULL -k regex:k_tile2 -s 2 -c 1 -o $O/${R}_edm_c2 -f \
     python scripts/one.py --m 2 --n 65536 --payload edm --rho 256 --gran tile --layout tiles --flags 4 --reps 3 > /dev/null 2>&1
 $FULL -k regex:k_tile3 -s 2 -c 1 -o $O/${R}_iwa_c3 -f \
     python scripts/one.py --m 3 --n 1024 --payload index_write_atm --param 0.01 --rho 32 --gran tile --layout tiles --flags 4 --reps 3 > /dev/null 2>&1
+$FULL -k regex:k_tile3 -s 2 -c 1 -o $O/${R}_iw_c3 -f \
+    python scripts/one.py --m 3 --n 1024 --payload index_write --rho 32 --gran tile --layout tiles --flags 4 --reps 3 > /dev/null 2>&1
 $FULL -k regex:k_tile3 -s 2 -c 1 -o $O/${R}_atm_c3 -f \
     python scripts/one.py --m 3 --n 1024 --payload atm --param 0.01 --rho 32 --gran tile --reps 3 > /dev/null 2>&1
 $FULL -k regex:k_tile3 -s 2 -c 1 -o $O/${R}_tc_c5 -f \
@@ -32,8 +34,8 @@ cp $O/shards.json $O/${R}_shard_emulation.json 2>/dev/null
 python scripts/sustained.py > $O/${R}_sustained.log 2>&1
 cp $O/sustained.json $O/${R}_sustained_power_cap.json 2>/dev/null
 # summaries here (ncu is on the box); the large reports stay behind (gpurun_out <= 64 MiB)
-for k in edm_c2 iwa_c3 atm_c3 tc_c5 iw_c4; do
+for k in edm_c2 iwa_c3 iw_c3 atm_c3 tc_c5 iw_c4; do
     python scripts/ncu_summary.py $O/${R}_$k.ncu-rep $O/${R}_${k}_ncu_full.json > /dev/null 2>&1
 done
-rm -f $O/${R}_edm_c2.ncu-rep $O/${R}_iw_c4.ncu-rep $O/${R}_iwa_c3.ncu-rep
+rm -f $O/${R}_*.ncu-rep
 ls -la $O | tail -30
