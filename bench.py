@@ -325,10 +325,10 @@ def sharded_configs(ctx, golden):
         plan = sm.smap_plan(m, n, shard_rank=ctx.rank, shard_count=ctx.G, device=ctx.local, **launch)
         pts = torch.from_numpy(workloads.points(n, seed)).to(ctx.dev) if seed else None
         out = sm.alloc_out(plan, payload, device=ctx.dev)
-        # the step's fused reduction: count + xor for the index write (C4); count + the ATM sum
-        # for C3 (the xor of the ranks 0 .. V-1 is 0, so C3 skips it); count + tc for C5
-        flags = sm.RUN_XOR if payload == "index_write" else 0
-        step_ms, kern_ms, _, launches = shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps)
+        # the step's fused reduction: count + xor for the index writes (C4, and C3 with its ATM
+        # sum: E21', the bench's reduction for every write payload); count + tc for C5
+        flags = sm.RUN_XOR if payload in ("index_write", "index_write_atm") else 0
+        step_ms, kern_ms, timed_rec, launches = shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps)
         step_max, kern_max = ctx.max_over_ranks(step_ms, kern_ms)
         (kern_min,) = ctx.min_over_ranks(kern_ms)
         # verification step (untimed): count + s0 (index writes; their xr of 0 .. V-1 is 0) / ATM sum / TC count
@@ -343,6 +343,11 @@ def sharded_configs(ctx, golden):
         if "tc" in g:
             ok = ok and rec["tc"] == g["tc"]
         V = g["count"]
+        if flags & sm.RUN_XOR:
+            # the timed steps' own record: the index-write values are the ranks 0 .. V-1, whose xor
+            # has the closed form [m, 1, m+1, 0][m mod 4] for m = V - 1
+            m = V - 1
+            ok = ok and timed_rec["count"] == V and timed_rec["xr"] == [m, 1, m + 1, 0][m % 4]
         e = {"launch": launch, "flags": flags, "kernels_per_step": launches,
              "ms_per_step": round(step_max, 4), "kernel_ms_max": round(kern_max, 4),
              "kernel_ms_min": round(kern_min, 4), "kernel_max_over_min": round(kern_max / kern_min, 3),

@@ -37,7 +37,7 @@ def main():
         m, payload, seed, param = CASES[name]
         n = workloads.C5X["n"] if name == "C5X" else workloads.CONFIGS[name]["n"]
         pts = torch.from_numpy(workloads.points(n, seed)).cuda() if seed else None
-        flags = sm.RUN_XOR if payload in ("edm", "index_write") else 0
+        flags = sm.RUN_XOR if payload in ("edm", "index_write", "index_write_atm") else 0
         row = {"config": name, "n": n, "payload": payload, "ranks": {}}
         for G in (int(g) for g in a.gs.split(",")):
             launch = workloads.sharded_launch(name, G)
