@@ -76,6 +76,36 @@ def main():
                     flags=sm.RUN_XOR if pl != "tc" else 0)
         sm.smap_stats_fetch(plan)
         runs += 1
+    # round 2: SMAP_RUN_FAST_SQRT (incl. the staging fallback), the symmetric TC pre-pass at
+    # T = 64 with a padded n, and lean CUDA-graph steps (record folded into the finalize,
+    # programmatic-dependent tail kernels, result block cleared behind the record)
+    for scale in (1.0, 1e-15):
+        pts = torch.from_numpy((workloads.points(1024, 7) * scale).astype("float32")).cuda()
+        plan = sm.smap_plan(2, 1024, 256, granularity="tile", layout="tiles")
+        out = sm.alloc_out(plan, "edm")
+        sm.smap_run(plan, "edm", points=pts, out=out, flags=sm.RUN_XOR | sm.RUN_FAST_SQRT)
+        sm.smap_stats_fetch(plan)
+        runs += 1
+    for n in (1000, 1024):
+        pts = torch.from_numpy(workloads.points(n, 8)).cuda()
+        plan = sm.smap_plan(3, n, 64, granularity="tile", persistent=8)
+        sm.smap_run(plan, "tc", points=pts, param=0.5)
+        sm.smap_stats_fetch(plan)
+        runs += 1
+    rec = torch.zeros(7, dtype=torch.int64, device="cuda")
+    for m, n, kw, pl in ((3, 512, workloads.BENCH_C3, "index_write_atm"), (3, 512, workloads.BENCH_M3, "atm"),
+                         (3, 1024, workloads.BENCH_C5, "tc"), (2, 2048, workloads.BENCH_C4, "index_write")):
+        pts = torch.from_numpy(workloads.points(n, 9)).cuda() if pl != "index_write" else None
+        plan = sm.smap_plan(m, n, **kw)
+        out = sm.alloc_out(plan, pl)
+        g = sm.smap_graph_capture(plan, pl, points=pts, param=0.5 if pl == "tc" else 1e-2, out=out,
+                                  flags=sm.RUN_XOR if pl in ("index_write", "index_write_atm") else 0, record=rec)
+        for _ in range(2):
+            sm.smap_graph_launch(g)
+            runs += 1
+        sm.smap_run(plan, pl, points=pts, param=0.5 if pl == "tc" else 1e-2, out=out)   # leaves the block dirty
+        sm.smap_graph_launch(g)
+        runs += 2
     torch.cuda.synchronize()
     print(f"sanitize cases: {runs} runs ok")
 
