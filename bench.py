@@ -412,6 +412,23 @@ def sustained(ctx, plan, pts, out, steps):
     return res
 
 
+def ncu_pipes(kernel: str) -> dict | None:
+    """Issue / FMA-pipe fractions of a config's dominant kernel from the committed ncu
+    --set full summary (profiles/r*_<kernel>_ncu_full.json, the newest round's): the
+    counters a CUDA-event run cannot see, quoted with their source file."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r[0-9][0-9]_{kernel}_ncu_full.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    pct = lambda k: float(str(d.get(k, "nan")).split()[0])   # noqa: E731
+    return {"source": os.path.relpath(files[-1], ROOT), "kernel_ns": pct("gpu__time_duration.sum"),
+            "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "fma_pipe_pct": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+            "warp_inst_per_launch": pct("smsp__inst_executed.sum")}
+
+
 # ------------------------------------------------------------------ the per-config table (N = 1)
 def config_table(ctx, peak_gbs, f_sm_mhz, reps=10):
     """Device time of every BASELINE.json config's product launch next to the
@@ -510,6 +527,7 @@ def config_table(ctx, peak_gbs, f_sm_mhz, reps=10):
              index_write_alone_gbs=round(V3 * 4 / (t_iw * 1e-3) / 1e9, 1),
              atm_fp32_pipe_frac=round(V3 * 11 / (t_atm * 1e-3) / fp32_peak, 4),
              fused_fp32_pipe_frac=round(V3 * 11 / (e["lambda_ms"] * 1e-3) / fp32_peak, 4),
+             ncu_fused=ncu_pipes("iwa_c3"), ncu_atm=ncu_pipes("atm_c3"),
              pipe_note="FP32-pipe fraction = 11 FP32 lane-ops per triple (E27 term, packed f32x2) x triples / "
                        f"time / (148 SM x 128 lanes x {f_hz / 1e6:.0f} MHz)")
     th, _ = pair(3, n, "index_write_atm", dict(rho=8, granularity="thread"), pts=pts3, param=c3["eps2"], out=out,
@@ -534,7 +552,7 @@ def config_table(ctx, peak_gbs, f_sm_mhz, reps=10):
     pts5 = torch.from_numpy(workloads.points(n, workloads.SEED_C5)).to(ctx.dev)
     e, st = pair(3, n, "tc", {k: v for k, v in workloads.BENCH_C5.items() if k != "map"}, pts=pts5, param=c5["R"])
     e.update(bound="issue (AND + POPC per 64-triple word)", tc=st["tc"],
-             word_ops_per_s=math.comb(n, 3) / 64 / (e["lambda_ms"] * 1e-3))
+             word_ops_per_s=math.comb(n, 3) / 64 / (e["lambda_ms"] * 1e-3), ncu=ncu_pipes("tc_c5"))
     th, _ = pair(3, n, "tc", dict(rho=8, granularity="thread"), pts=pts5, param=c5["R"], k=max(3, reps // 2))
     res["C5"] = {"product": e, "paper_launch": th}
     # which launch meets the north-star lambda/BB targets (>= 1.8x m=2, >= 4.5x m=3)
