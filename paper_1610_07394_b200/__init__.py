@@ -241,6 +241,19 @@ def _device_buffer(plan: Plan, x, what: str, nbytes=None, fp32_points=False):
     return x.data_ptr(), _nbytes(x) if nbytes is None else int(nbytes)
 
 
+def _record_ptr(x, what: str, count: int = 1):
+    """Pointer of a DEVICE result-record buffer of `count` 56-byte records: a
+    contiguous CUDA tensor of at least 56 * count bytes, or a raw device
+    pointer (the caller vouches for its size).  Host arrays are refused."""
+    if x is None or isinstance(x, int):
+        return x
+    if not getattr(x, "is_cuda", False):
+        raise TypeError(f"{what} must be a CUDA tensor (7 int64 per record) or a raw device pointer")
+    if not x.is_contiguous() or _nbytes(x) < 56 * count:
+        raise ValueError(f"{what} must be contiguous with at least {56 * count} bytes (got {_nbytes(x)})")
+    return x.data_ptr()
+
+
 def smap_run(plan: Plan, payload: str, points=None, param: float = 0.0, out=None, flags: int = 0,
              stream=None, points_bytes=None, out_bytes=None):
     """Asynchronous launch on `stream` (default: torch's current stream).
@@ -301,7 +314,9 @@ def smap_graph_capture(plan: Plan, payload: str, points=None, param: float = 0.0
     tensor of 7 int64) into a CUDA graph; replay it with smap_graph_launch."""
     pp, pb = _device_buffer(plan, points, "points", points_bytes, fp32_points=True)
     op, ob = _device_buffer(plan, out, "out", out_bytes)
-    rp, _ = _device_buffer(plan, record, "record", None if record is None or not isinstance(record, int) else 56)
+    if record is not None and not isinstance(record, int):
+        _device_buffer(plan, record, "record")                # on the plan's device, contiguous
+    rp = _record_ptr(record, "record")
     h = _P()
     _check(_lib.smap_graph_capture(plan.handle, PAYLOAD[payload], pp, pb, float(param), op, ob, flags, rp,
                                    C.byref(h)))
@@ -326,14 +341,15 @@ def smap_result_reduce(plan: Plan, dst, stream=None):
     of 7 int64 (count, s0, s1, mix, tc, xr, bits of the fp64 sum) -- ready for
     an all-reduce of dst[:5] (exact mod 2^64), an xor of dst[5] and a sum of
     dst[6:].view(float64)."""
-    _check(_lib.smap_result_reduce(plan.handle, _ptr(dst), _stream(stream)))
+    _check(_lib.smap_result_reduce(plan.handle, _record_ptr(dst, "dst"), _stream(stream)))
 
 
 def smap_result_combine(records, count: int, dst, stream=None):
     """Asynchronously combine `count` device records (7 int64 each, contiguous)
     into `dst` (7 int64 on the device): the cross-rank step after an
     all-gather of every rank's smap_result_reduce output, in one kernel."""
-    _check(_lib.smap_result_combine(_ptr(records), int(count), _ptr(dst), _stream(stream)))
+    _check(_lib.smap_result_combine(_record_ptr(records, "records", max(int(count), 1)), int(count),
+                                    _record_ptr(dst, "dst"), _stream(stream)))
 
 
 def result_dict(rec) -> dict:

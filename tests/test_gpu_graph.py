@@ -110,3 +110,19 @@ def test_graph_interleaved_with_direct_runs(sm, m, n, kw, payload, param, mode):
             assert sm.smap_stats_fetch(plan)["count"] == results[-1]["count"]
     assert all(r == results[0] for r in results), results
     assert results[0]["count"] == sm.smap_volume(m, n)
+
+
+def test_record_buffers_checked_by_the_binding(sm):
+    plan = sm.smap_plan(2, 1024, 128, granularity="tile", layout="tiles")
+    out = sm.alloc_out(plan, "index_write")
+    small = torch.zeros(3, dtype=torch.int64, device="cuda")          # < 56 bytes
+    with pytest.raises(ValueError):
+        sm.smap_graph_capture(plan, "index_write", out=out, record=small)
+    sm.smap_run(plan, "index_write", out=out)
+    with pytest.raises(ValueError):
+        sm.smap_result_reduce(plan, small)
+    with pytest.raises(TypeError):
+        sm.smap_result_reduce(plan, np.zeros(7, np.int64))              # host buffer
+    with pytest.raises(ValueError):
+        sm.smap_result_combine(torch.zeros(7, dtype=torch.int64, device="cuda"), 2,
+                               torch.zeros(7, dtype=torch.int64, device="cuda"))   # 2 records need 112 bytes
