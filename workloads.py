@@ -47,7 +47,7 @@ BENCH_M3 = dict(rho=32, granularity="tile", map="lambda")
 BENCH_M3_VARIANTS = [BENCH_M3, dict(rho=8, granularity="thread", map="lambda")]
 BENCH_C3 = dict(rho=32, granularity="tile", map="lambda", layout="tiles")   # fused index write + ATM (E26)
 BENCH_C4 = dict(rho=128, granularity="tile", map="lambda", layout="tiles")
-BENCH_C5 = dict(rho=64, granularity="tile", map="lambda", persistent=8)   # TC: 64-bit predicate rows, 8 CTAs/SM
+BENCH_C5 = dict(rho=64, granularity="tile", map="lambda", persistent=16)   # TC: 64-bit predicate rows, 16 128-thread CTAs/SM
 
 
 def sharded_launch(name: str, G: int) -> dict:
