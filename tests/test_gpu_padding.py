@@ -130,3 +130,30 @@ def test_inclusive_m3_rejects_point_payloads(sm):
         sm.smap_run(plan, "atm", points=p, param=1e-2)
     with pytest.raises(Exception):
         sm.smap_run(plan, "tc", points=p, param=0.5)
+
+
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+@pytest.mark.parametrize("n", [777, 1000, 1024])
+@pytest.mark.parametrize("persistent", [0, 16])
+def test_tc_tile64_any_n(sm, orc, map_, n, persistent):
+    """The T = 64 TC tiles (128-thread CTAs, double-buffered bit rows, the symmetric
+    32 x 32-block bitmap pass) at padded and power-of-two n, persistent or not."""
+    p = workloads.points(n, 23)
+    plan = sm.smap_plan(3, n, 64, map=map_, granularity="tile", persistent=persistent)
+    _, st = run(sm, plan, "tc", points=dev(p), param=0.5)
+    assert st["count"] == math.comb(n, 3)
+    assert st["tc"] == orc.tc_count(p, np.float32(0.5))
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_tc_tile64_shards_add_up(sm, orc, G):
+    n = 1024
+    p = workloads.points(n, 29)
+    tot = cnt = 0
+    for r in range(G):
+        plan = sm.smap_plan(3, n, 64, granularity="tile", persistent=16, shard_rank=r, shard_count=G)
+        _, st = run(sm, plan, "tc", points=dev(p), param=0.5)
+        tot += st["tc"]
+        cnt += st["count"]
+    assert cnt == math.comb(n, 3)
+    assert tot == orc.tc_count(p, np.float32(0.5))
