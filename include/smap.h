@@ -139,7 +139,9 @@ typedef struct {
     int     map;          /* smap_map */
     int     diag;         /* smap_diag */
     int     granularity;  /* smap_granularity */
-    int     persistent;   /* TILE only: 0 = one CTA per tile; k > 0 = k CTAs per SM looping over tiles */
+    int     persistent;   /* TILE only: 0 = one CTA per tile; k > 0 = k CTAs per SM looping over tiles.
+                           * CTAs have 256 threads, except TC at rho = 64: 128 threads, or 64 when
+                           * k >= 32 (the sizes that fill an SM at 16 / 32 CTAs) */
     int     shard_rank;   /* 0 .. shard_count-1 */
     int     shard_count;  /* G: power of two dividing N/2 (lambda only); 1 = unsharded */
     int     device;       /* CUDA device ordinal; -1 = the calling thread's current device;

@@ -440,6 +440,7 @@ static smap_status run_prepare(smap_plan_t p, smap_payload pl, const float *poin
     a->P.pts = points;
     a->P.param = param;
     a->P.fsqrt = (flags & SMAP_RUN_FAST_SQRT) ? 1 : 0;
+    a->P.tc64 = (ipl == PL_TC && tile && d.rho == 64 && d.persistent >= 32) ? 1 : 0;
     a->P.out = out;
     a->P.partials = p->d_partials;
     a->P.adj = p->d_adj;

@@ -64,6 +64,7 @@ struct Params {
     const Piece *pieces;           // SMAP_MAP_BELOW: the decomposition, sorted by start
     int npieces;
     int fsqrt;                     // EDM (SMAP_RUN_FAST_SQRT): sqrt.approx on the vector tile path
+    int tc64;                      // TC, T = 64: 64-thread CTAs (plans with >= 32 persistent CTAs per SM)
 };
 
 // ---------------------------------------------------------------- m=3 tile-blocked layout (E26)

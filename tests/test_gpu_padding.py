@@ -157,3 +157,14 @@ def test_tc_tile64_shards_add_up(sm, orc, G):
         cnt += st["count"]
     assert cnt == math.comb(n, 3)
     assert tot == orc.tc_count(p, np.float32(0.5))
+
+
+@pytest.mark.parametrize("map_", ["lambda", "bb"])
+@pytest.mark.parametrize("n", [1000, 2048])
+def test_tc_tile64_64thread_ctas(sm, orc, map_, n):
+    """persistent >= 32 selects the 64-thread TC CTAs (64 k rows per thread)."""
+    p = workloads.points(n, 31)
+    plan = sm.smap_plan(3, n, 64, map=map_, granularity="tile", persistent=32)
+    _, st = run(sm, plan, "tc", points=dev(p), param=0.5)
+    assert st["count"] == math.comb(n, 3)
+    assert st["tc"] == orc.tc_count(p, np.float32(0.5))

@@ -48,12 +48,13 @@ BENCH_M3_VARIANTS = [BENCH_M3, dict(rho=8, granularity="thread", map="lambda")]
 BENCH_C3 = dict(rho=32, granularity="tile", map="lambda", layout="tiles")   # fused index write + ATM (E26)
 BENCH_C4 = dict(rho=128, granularity="tile", map="lambda", layout="tiles")
 BENCH_C5 = dict(rho=64, granularity="tile", map="lambda", persistent=16)   # TC: 64-bit predicate rows, 16 128-thread CTAs/SM
+BENCH_C5X = dict(rho=64, granularity="tile", map="lambda", persistent=32)  # n = 8192: 32 64-thread CTAs/SM (many tiles each)
 
 
 def sharded_launch(name: str, G: int) -> dict:
     """smap_plan keyword arguments of config `name`'s product launch on one of
     G omega_x shards (bench.py configs_sharded)."""
-    base = {"C2": BENCH_EDM, "C3": BENCH_C3, "C4": BENCH_C4, "C5": BENCH_C5, "C5X": BENCH_C5}[name]
+    base = {"C2": BENCH_EDM, "C3": BENCH_C3, "C4": BENCH_C4, "C5": BENCH_C5, "C5X": BENCH_C5X}[name]
     return dict(base)
 
 
