@@ -29,6 +29,9 @@ struct smap_plan_s {
     uint64_t npartials = 0;
     double *d_scratch = nullptr;
     uint32_t *d_adj = nullptr;      // TC pair-predicate bitmap (TILE)
+    uint32_t *d_tcpairs = nullptr;  // TC, sharded lambda plan: the bitmap block pairs this shard reads
+    uint32_t ntcpairs = 0;
+    int tcpairs_done = 0;           // (the shard analysis ran; d_tcpairs null = build every pair)
     Piece *d_pieces = nullptr;      // SMAP_MAP_BELOW decomposition
     std::vector<uint32_t> segN, segO;   // SMAP_MAP_BELOW: the binary-digit segments of M (sizes, offsets)
     uint64_t layout_len = 0;        // SMAP_MAP_BELOW tile-blocked layout: slots incl. holes (E29)
@@ -371,6 +374,52 @@ struct RunArgs {
     Params P;
 };
 
+// TC shard analysis (once per sharded lambda3 TILE plan, T = 32 / 64): enumerate the
+// shard's tiles with the kernels' own decode and list the 32 x 32 blocks of the pair
+// bitmap they read -- tables (I,J) (I,K) and the transposed (K,J) of an interior tile,
+// (I,I) (I,K) (K,I) (K,K) of a face tile, (I,I) of a body tile, as (row block, word
+// block) -- folded to unordered pairs (the pre-pass writes both orientations).  At
+// G = 8 a shard reads 27-46 % of the bitmap (n = 8192).  Unsharded plans, other T and
+// grids of more than 2^22 tiles keep the full pre-pass.
+static smap_status tc_shard_pairs(smap_plan_t p)
+{
+    p->tcpairs_done = 1;
+    const smap_plan_desc &d = p->d;
+    const uint64_t T = (uint64_t)d.rho;
+    if (d.map != SMAP_MAP_LAMBDA || d.shard_count <= 1 || (T != 32 && T != 64) || p->P.nblocks > ((uint64_t)1 << 22))
+        return SMAP_OK;
+    const uint64_t W32 = (uint64_t)p->P.N * T / 32, s = T / 32;          // 32-blocks per side, per tile block
+    std::vector<uint8_t> need(W32 * W32, 0);
+    auto mark = [&](uint64_t Y, uint64_t X) {           // tile-block pair (row block Y, word block X)
+        for (uint64_t a = 0; a < s; a++)
+            for (uint64_t b = 0; b < s; b++) {
+                const uint64_t r = Y * s + a, c = X * s + b;
+                need[(r > c ? r : c) * W32 + (r > c ? c : r)] = 1;
+            }
+    };
+    for (uint64_t bid = 0; bid < p->P.nblocks; bid++) {
+        const Blk3 B = decode_lambda3(bid, p->P);
+        if (B.cls == 3) continue;
+        if (B.cls == 2) { mark(B.I, B.I); continue; }
+        if (B.I < B.J) { mark(B.J, B.I); mark(B.K, B.I); mark(B.J, B.K); }
+        else { mark(B.I, B.I); mark(B.K, B.I); mark(B.I, B.K); mark(B.K, B.K); }
+    }
+    std::vector<uint32_t> list;
+    for (uint64_t r = 0; r < W32; r++)
+        for (uint64_t c = 0; c <= r; c++)
+            if (need[r * W32 + c]) list.push_back((uint32_t)(r << 16 | c));
+    if (list.size() == W32 * (W32 + 1) / 2) return SMAP_OK;   // every pair: the plain pass
+    if (!list.empty()) {
+        CK(cudaMalloc(&p->d_tcpairs, list.size() * sizeof(uint32_t)));
+        CK(cudaMemcpy(p->d_tcpairs, list.data(), list.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
+    p->ntcpairs = (uint32_t)list.size();
+    if (list.empty()) {                                  // (a shard with no tile: keep a valid non-null marker)
+        CK(cudaMalloc(&p->d_tcpairs, sizeof(uint32_t)));
+    }
+    return SMAP_OK;
+}
+
 // Validation and the plan's lazily allocated scratch (TC bitmap, ATM partials); the
 // plan's device must be current.  No device work is queued.
 static smap_status run_prepare(smap_plan_t p, smap_payload pl, const float *points, size_t points_bytes, float param,
@@ -425,6 +474,10 @@ static smap_status run_prepare(smap_plan_t p, smap_payload pl, const float *poin
     const bool tc_bits = ipl == PL_TC && tile;
     const int64_t npad = (int64_t)p->P.N * d.rho;          // bitmap over the grid's index range
     if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)npad * (size_t)((npad + 31) / 32) * sizeof(uint32_t)));
+    if (tc_bits && !p->tcpairs_done) {
+        smap_status st = tc_shard_pairs(p);
+        if (st != SMAP_OK) return st;
+    }
     if (atm) {
         const uint64_t np = tile ? p->ctas : p->P.nblocks;
         if (np > p->npartials) {
@@ -464,7 +517,8 @@ static smap_status run_launch(smap_plan_t p, const RunArgs &a, cudaStream_t s, b
     if (timed) CK(cudaEventRecord(p->ev0, s));
     cudaError_t e;
     if (a.tc_bits) {
-        cudaError_t ea = launch_tc_adjacency(a.P.pts, (int)d.n, (int)a.npad, a.P.param, p->d_adj, p->d_res, s);
+        cudaError_t ea = launch_tc_adjacency(a.P.pts, (int)d.n, (int)a.npad, a.P.param, p->d_adj, p->d_res,
+                                             p->d_tcpairs, p->ntcpairs, s);
         if (ea != cudaSuccess) return cuda_fail(ea, "TC adjacency launch");
         launches++;
     }
@@ -897,6 +951,7 @@ void smap_destroy(smap_plan_t p)
     if (p->d_partials) cudaFree(p->d_partials);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_adj) cudaFree(p->d_adj);
+    if (p->d_tcpairs) cudaFree(p->d_tcpairs);
     if (p->d_pieces) cudaFree(p->d_pieces);
     if (p->d_stage) cudaFree(p->d_stage);
     if (p->d_rec) cudaFree(p->d_rec);

@@ -146,7 +146,10 @@ cudaError_t launch_tile3(const Params &P, int T, int map, int pl, int cs, unsign
 // r2(32w + b, j) < R*R (the same fp32 predicate as the per-triple compare);
 // npad = N * rho (rows j < npad, words rounded up).
 // It also zeroes the run's result block (the main kernel follows in stream order).
-cudaError_t launch_tc_adjacency(const float *pts, int n, int npad, float R, uint32_t *adj, Result *res, cudaStream_t s);
+// pairs (optional): the list of 32 x 32 block pairs (rb << 16 | cb, cb <= rb) to build
+// (a sharded plan builds only what its tiles read); null = all of them.
+cudaError_t launch_tc_adjacency(const float *pts, int n, int npad, float R, uint32_t *adj, Result *res,
+                                const uint32_t *pairs, uint32_t npairs, cudaStream_t s);
 uint64_t finalize_scratch_elems(uint64_t np);
 }  // namespace smap
 

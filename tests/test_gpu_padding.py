@@ -146,12 +146,15 @@ def test_tc_tile64_any_n(sm, orc, map_, n, persistent):
 
 
 @pytest.mark.parametrize("G", [2, 4, 8])
-def test_tc_tile64_shards_add_up(sm, orc, G):
+@pytest.mark.parametrize("rho,persistent", [(64, 16), (64, 32), (32, 8)])
+def test_tc_tile64_shards_add_up(sm, orc, G, rho, persistent):
+    """Sharded TC plans build only the bitmap blocks their tiles read (the plan's
+    shard analysis); the shard counts must still add up to the oracle's count."""
     n = 1024
     p = workloads.points(n, 29)
     tot = cnt = 0
     for r in range(G):
-        plan = sm.smap_plan(3, n, 64, granularity="tile", persistent=16, shard_rank=r, shard_count=G)
+        plan = sm.smap_plan(3, n, rho, granularity="tile", persistent=persistent, shard_rank=r, shard_count=G)
         _, st = run(sm, plan, "tc", points=dev(p), param=0.5)
         tot += st["tc"]
         cnt += st["count"]
