@@ -473,7 +473,8 @@ static smap_status run_prepare(smap_plan_t p, smap_payload pl, const float *poin
 
     const bool tc_bits = ipl == PL_TC && tile;
     const int64_t npad = (int64_t)p->P.N * d.rho;          // bitmap over the grid's index range
-    if (tc_bits && !p->d_adj) CK(cudaMalloc(&p->d_adj, (size_t)npad * (size_t)((npad + 31) / 32) * sizeof(uint32_t)));
+    if (tc_bits && !p->d_adj)      // 32-row x 64-column blocks (adj_word, smap_tile3.cu)
+        CK(cudaMalloc(&p->d_adj, (size_t)((npad + 31) / 32) * (size_t)(((npad + 31) / 32 + 1) / 2) * 256));
     if (tc_bits && !p->tcpairs_done) {
         smap_status st = tc_shard_pairs(p);
         if (st != SMAP_OK) return st;
