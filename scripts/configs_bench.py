@@ -127,7 +127,8 @@ def main():
         p = torch.from_numpy(workloads.points(n, workloads.SEED_C5)).cuda()
         var = [("thread_rho8", dict(rho=8, granularity="thread")), ("tile_rho16", dict(rho=16, granularity="tile")),
                ("tile_rho32", dict(rho=32, granularity="tile")), ("tile_rho64", dict(rho=64, granularity="tile")),
-               ("tile_rho64_p16", dict(rho=64, granularity="tile", persistent=16))]
+               ("tile_rho64_p16", dict(rho=64, granularity="tile", persistent=16)),
+               ("tile_rho64_p32", dict(rho=64, granularity="tile", persistent=32))]
         table["configs"]["C5"] = compare(3, n, "tc", var, pts=p, param=0.5, reps=a.reps)
     torch.cuda.empty_cache()
     os.makedirs("gpurun_out", exist_ok=True)

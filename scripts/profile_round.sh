@@ -22,7 +22,7 @@ $FULL -k regex:k_tile3 -s 2 -c 1 -o $O/${R}_iw_c3 -f \
 $FULL -k regex:k_tile3 -s 2 -c 1 -o $O/${R}_atm_c3 -f \
     python scripts/one.py --m 3 --n 1024 --payload atm --param 0.01 --rho 32 --gran tile --reps 3 > /dev/null 2>&1
 $FULL -k regex:k_tile3 -s 2 -c 1 -o $O/${R}_tc_c5 -f \
-    python scripts/one.py --m 3 --n 2048 --payload tc --param 0.5 --rho 64 --gran tile --persistent 16 --reps 3 > /dev/null 2>&1
+    python scripts/one.py --m 3 --n 2048 --payload tc --param 0.5 --rho 64 --gran tile --persistent 32 --reps 3 > /dev/null 2>&1
 $FULL -k regex:k_tile2 -s 2 -c 1 -o $O/${R}_iw_c4 -f \
     python scripts/one.py --m 2 --n 131072 --payload index_write --rho 128 --gran tile --layout tiles --flags 4 --reps 3 > /dev/null 2>&1
 python scripts/configs_bench.py > $O/${R}_configs.log 2>&1

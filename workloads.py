@@ -47,15 +47,25 @@ BENCH_M3 = dict(rho=32, granularity="tile", map="lambda")
 BENCH_M3_VARIANTS = [BENCH_M3, dict(rho=8, granularity="thread", map="lambda")]
 BENCH_C3 = dict(rho=32, granularity="tile", map="lambda", layout="tiles")   # fused index write + ATM (E26)
 BENCH_C4 = dict(rho=128, granularity="tile", map="lambda", layout="tiles")
-BENCH_C5 = dict(rho=64, granularity="tile", map="lambda", persistent=16)   # TC: 64-bit predicate rows, 16 128-thread CTAs/SM
-BENCH_C5X = dict(rho=64, granularity="tile", map="lambda", persistent=32)  # n = 8192: 32 64-thread CTAs/SM (many tiles each)
+# TC: 64-bit predicate rows; persistent >= 32 selects 64-thread CTAs (32 resident per SM).
+# C5 (6144 tiles): one resident round of 32 CTAs/SM; C5X (n = 8192, 393K tiles): 256 per
+# SM, i.e. 8 rounds the block scheduler hands out as CTAs finish -- dynamic balance over
+# tiles of unequal cost (face tiles stage four bit tables), measured faster than one
+# resident round at every G (profiles/r02_ab_tc_prepass_steps.log)
+BENCH_C5 = dict(rho=64, granularity="tile", map="lambda", persistent=32)
+BENCH_C5X = dict(rho=64, granularity="tile", map="lambda", persistent=256)
 
 
 def sharded_launch(name: str, G: int) -> dict:
     """smap_plan keyword arguments of config `name`'s product launch on one of
     G omega_x shards (bench.py configs_sharded)."""
     base = {"C2": BENCH_EDM, "C3": BENCH_C3, "C4": BENCH_C4, "C5": BENCH_C5, "C5X": BENCH_C5X}[name]
-    return dict(base)
+    launch = dict(base)
+    if name == "C5" and G > 1:
+        # a shard has 6144 / G tiles: fewer than one per 64-thread CTA slot at G >= 2, where
+        # 16 resident 128-thread CTAs per SM (half the k rows per thread) finish sooner
+        launch["persistent"] = 16
+    return launch
 
 
 def points(n: int, seed: int) -> np.ndarray:
