@@ -92,6 +92,15 @@ def main():
         sm.smap_run(plan, "tc", points=pts, param=0.5)
         sm.smap_stats_fetch(plan)
         runs += 1
+    # round 2 (late): the rewritten pair-bitmap pre-pass (blocked layout, warp bit transpose)
+    # unsharded and with the shard block lists, T = 32 / 64, all three TC CTA sizes, padded n
+    for n, rho, persistent, G in ((1000, 64, 32, 1), (1000, 64, 16, 3), (1000, 32, 0, 2), (777, 64, 256, 2)):
+        pts = torch.from_numpy(workloads.points(n, 10)).cuda()
+        for r in range(G):
+            plan = sm.smap_plan(3, n, rho, granularity="tile", persistent=persistent, shard_rank=r, shard_count=G)
+            sm.smap_run(plan, "tc", points=pts, param=0.5)
+            sm.smap_stats_fetch(plan)
+            runs += 1
     rec = torch.zeros(7, dtype=torch.int64, device="cuda")
     for m, n, kw, pl in ((3, 512, workloads.BENCH_C3, "index_write_atm"), (3, 512, workloads.BENCH_M3, "atm"),
                          (3, 1024, workloads.BENCH_C5, "tc"), (2, 2048, workloads.BENCH_C4, "index_write")):
