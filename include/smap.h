@@ -100,9 +100,9 @@ typedef enum {
     SMAP_PAYLOAD_EDM = 1,         /* m=2 strict: out[p] = ||x_i - x_j||_2, fp32 (E15, E17) */
     SMAP_PAYLOAD_ATM = 2,         /* m=3: sum of Axilrod-Teller terms (E15), param = eps^2; result stats.sum */
     SMAP_PAYLOAD_TC = 3,          /* m=3: #{i<j<k: r_ij, r_jk, r_ik < R}, param = R; result stats.tc.  TILE plans
-                                     allocate an n'^2 / 8-byte pair-predicate bitmap in the plan's scratch on
-                                     the first TC run (n' = the grid's index range; SMAP_E_NOMEM if it does
-                                     not fit) */
+                                     allocate a pair-predicate bitmap of ~n'^2 / 8 bytes (32-row x 64-column
+                                     blocks, n' rounded up to them) in the plan's scratch on the first TC run
+                                     (n' = the grid's index range; SMAP_E_NOMEM if it does not fit) */
     SMAP_PAYLOAD_MAP_DUMP = 4,    /* int32[4] per grid block/tile in launch order (see below) */
     SMAP_PAYLOAD_HITCOUNT = 5,    /* uint32 out[p] += 1 per mapped element (caller zeroes out) */
     SMAP_PAYLOAD_THREAD_DUMP = 6, /* THREAD gran. only: uint64 per launched thread, p or UINT64_MAX */
@@ -139,7 +139,9 @@ typedef struct {
     int     map;          /* smap_map */
     int     diag;         /* smap_diag */
     int     granularity;  /* smap_granularity */
-    int     persistent;   /* TILE only: 0 = one CTA per tile; k > 0 = k CTAs per SM looping over tiles.
+    int     persistent;   /* TILE only: 0 = one CTA per tile; k > 0 = k CTAs per SM looping over tiles
+                           * (grid-stride; k above the resident limit launches the extra CTAs as
+                           * others finish -- dynamic balance over tiles of unequal cost).
                            * CTAs have 256 threads, except TC at rho = 64: 128 threads, or 64 when
                            * k >= 32 (the sizes that fill an SM at 16 / 32 CTAs) */
     int     shard_rank;   /* 0 .. shard_count-1 */
