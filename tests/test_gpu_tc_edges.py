@@ -62,3 +62,37 @@ def test_tc_ties_sharded(sm, orc, G):
     p = lattice_points(n, 43)
     want = orc.tc_count(p, np.float32(0.5))
     assert tc(sm, n, p, np.float32(0.5), 64, 16, G) == want
+
+
+# ---- large bitmaps (>= 128 blocks per side: C5X size)
+def _golden_c5x():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "bench_expected.json")) as f:
+        return json.load(f)["C5X"]
+
+
+@pytest.mark.parametrize("G,persistent", [(1, 256), (8, 256), (2, 16)])
+def test_c5x_full_size(sm, G, persistent):
+    """C5X (n = 8192, the supplementary scaling workload) at full size, unsharded and
+    sharded: the shard counts add up to the oracle-written golden count
+    (tests/golden/bench_expected.json, scripts/make_bench_golden.py)."""
+    import workloads
+    g = _golden_c5x()
+    p = workloads.points(g["n"], g["seed"])
+    assert tc(sm, g["n"], p, np.float32(g["R"]), 64, persistent, G) == g["tc"]
+
+
+@pytest.mark.parametrize("map_,n", [("lambda", 4100), ("bb", 4096)])
+def test_large_bitmap_vs_oracle(sm, orc, map_, n):
+    """The pre-pass and the 64-thread count at n > 4096 (a padded n: the last bitmap
+    blocks partly outside the point set) and with the BB map, against the oracle's
+    brute-force count."""
+    import workloads
+    p = workloads.points(n, 47)
+    d = torch.from_numpy(p).cuda()
+    plan = sm.smap_plan(3, n, 64, map=map_, granularity="tile", persistent=32)
+    sm.smap_run(plan, "tc", points=d, param=0.5)
+    st = sm.smap_stats_fetch(plan)
+    assert st["count"] == math.comb(n, 3)
+    assert st["tc"] == orc.tc_count(p, np.float32(0.5))
