@@ -277,8 +277,8 @@ def shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps, warm=2):
     rank's part of the step -- the payload kernels and the record reduction --
     is one CUDA graph (smap_graph_capture: no host enqueue between its
     kernels); step = graph + (G > 1) the all-gather of the 56-byte records +
-    the combine kernel.  Returns (median step ms, median graph ms, combined
-    record, kernels per step)."""
+    the combine kernel.  Returns (mean step ms over `reps` back-to-back steps,
+    median graph ms, combined record, kernels per step)."""
     torch, sm, s = ctx.torch, ctx.sm, ctx.stream
     rec = torch.zeros(7, dtype=torch.int64, device=ctx.dev)
     gathered = torch.zeros(ctx.G * 7, dtype=torch.int64, device=ctx.dev)
@@ -297,14 +297,22 @@ def shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps, warm=2):
     for _ in range(warm):
         step()
     ctx.barrier()
-    ev = [(ctx.event(), ctx.event(), ctx.event(), ctx.event()) for _ in range(reps)]
-    for a, ka, kb, b in ev:
-        a.record(s)
-        step(ka, kb)
-        b.record(s)
+    # the step time: `reps` steps enqueued back to back between two events (as the
+    # headline's timed region), so a step of a few microseconds is not stretched by
+    # per-step event records; then the graph-only time per step from events around
+    # each graph launch, in a second pass
+    a, b = ctx.event(), ctx.event()
+    a.record(s)
+    for _ in range(reps):
+        step()
+    b.record(s)
     ctx.barrier()
-    step_ms = statistics.median(a.elapsed_time(b) for a, _, _, b in ev) if reps else 0.0
-    kern_ms = statistics.median(ka.elapsed_time(kb) for _, ka, kb, _ in ev) if reps else 0.0
+    step_ms = a.elapsed_time(b) / reps if reps else 0.0
+    ev = [(ctx.event(), ctx.event()) for _ in range(reps)]
+    for ka, kb in ev:
+        step(ka, kb)
+    ctx.barrier()
+    kern_ms = statistics.median(ka.elapsed_time(kb) for ka, kb in ev) if reps else 0.0
     launches = graph.launches + (1 if ctx.G > 1 else 0)
     return step_ms, kern_ms, ctx.sm.result_dict(rec), launches
 
@@ -349,6 +357,9 @@ def sharded_configs(ctx, golden):
             m = V - 1
             ok = ok and timed_rec["count"] == V and timed_rec["xr"] == [m, 1, m + 1, 0][m % 4]
         e = {"launch": launch, "flags": flags, "kernels_per_step": launches,
+             "timing": "ms_per_step: reps steps back to back between two events, max over ranks; "
+                       "kernel_ms_*: events around each graph launch in a second pass (includes the "
+                       "launch's submission gap when a step is shorter than the host's enqueue)",
              "ms_per_step": round(step_max, 4), "kernel_ms_max": round(kern_max, 4),
              "kernel_ms_min": round(kern_min, 4), "kernel_max_over_min": round(kern_max / kern_min, 3),
              "elements_per_s": V / (step_max * 1e-3), "elements_per_s_kernel": V / (kern_max * 1e-3),
