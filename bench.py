@@ -317,6 +317,41 @@ def shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps, warm=2):
     return step_ms, kern_ms, ctx.sm.result_dict(rec), launches
 
 
+def two_plan_timing(ctx, m, n, launch, payload, pts, param, flags, reps):
+    """N = 1 only: the same step on two plans (two scratch sets and outputs), launched
+    alternately on two streams, so that step k+1's first kernels overlap step k's
+    last ones (the usage for a stream of batches); mean ms per step over `reps`
+    steps between two events, and the records of the last two steps."""
+    torch, sm = ctx.torch, ctx.sm
+    s0, s1 = ctx.stream, torch.cuda.Stream(device=ctx.dev)
+    gs = []
+    for _ in range(2):
+        plan = sm.smap_plan(m, n, device=ctx.local, **launch)
+        out = sm.alloc_out(plan, payload, device=ctx.dev)
+        rec = torch.zeros(7, dtype=torch.int64, device=ctx.dev)
+        gs.append((plan, out, rec, sm.smap_graph_capture(plan, payload, points=pts, param=param, out=out,
+                                                         flags=flags, record=rec)))
+
+    def run(k):
+        e0, e1 = ctx.event(), ctx.event()
+        e0.record(s0)
+        s1.wait_event(e0)
+        for i in range(k):
+            sm.smap_graph_launch(gs[i % 2][3], stream=s0 if i % 2 == 0 else s1)
+        j = ctx.torch.cuda.Event()
+        j.record(s1)
+        s0.wait_event(j)
+        e1.record(s0)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / max(k, 1)
+
+    run(4)
+    ms = run(reps)
+    recs = [sm.result_dict(g[2]) for g in gs]
+    del gs
+    return ms, recs
+
+
 def sharded_configs(ctx, golden):
     """C3, C4, C5 (+ the n = 8192 supplementary C5) at this run's N: every rank
     runs its omega_x shard; max over ranks; checked against the
@@ -354,8 +389,8 @@ def sharded_configs(ctx, golden):
         if flags & sm.RUN_XOR:
             # the timed steps' own record: the index-write values are the ranks 0 .. V-1, whose xor
             # has the closed form [m, 1, m+1, 0][m mod 4] for m = V - 1
-            m = V - 1
-            ok = ok and timed_rec["count"] == V and timed_rec["xr"] == [m, 1, m + 1, 0][m % 4]
+            mv = V - 1
+            ok = ok and timed_rec["count"] == V and timed_rec["xr"] == [mv, 1, mv + 1, 0][mv % 4]
         e = {"launch": launch, "flags": flags, "kernels_per_step": launches,
              "timing": "ms_per_step: reps steps back to back between two events, max over ranks; "
                        "kernel_ms_*: events around each graph launch in a second pass (includes the "
@@ -366,6 +401,21 @@ def sharded_configs(ctx, golden):
              "checked_vs_oracle": bool(ok)}
         if payload == "index_write":
             e["achieved_gbs_kernel"] = round(V * 8 / ctx.G / (kern_max * 1e-3) / 1e9, 1)
+        if ctx.G == 1 and name != "C4":
+            # two steps in flight (two plans, two streams): every step's record checked
+            tms, recs = two_plan_timing(ctx, m, n, launch, payload, pts, param, flags, 2 * reps)
+            tok = all(r["count"] == V for r in recs)
+            if flags & sm.RUN_XOR:
+                tok = tok and all(r["xr"] == [V - 1, 1, V, 0][(V - 1) % 4] for r in recs)
+            if "tc" in g:
+                tok = tok and all(r["tc"] == g["tc"] for r in recs)
+            if "atm_sum" in g:
+                tok = tok and all(abs(r["sum"] - g["atm_sum"]) <= 1e-5 * abs(g["atm_sum"]) for r in recs)
+            e["two_plans"] = {"ms_per_step": round(tms, 4), "elements_per_s": V / (tms * 1e-3),
+                              "checked_vs_oracle": bool(tok),
+                              "what": "N = 1: the step on two plans (two pair bitmaps / result blocks / outputs) "
+                                      "alternating over two streams, steps back to back: a step's pre-pass and "
+                                      "first tiles overlap the previous step's tail (a stream of batches)"}
         if name == "C5X":
             e["note"] = "supplementary scaling workload (n=8192, 64x the triples of C5), not a BASELINE config"
         res[name] = e
