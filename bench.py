@@ -318,35 +318,49 @@ def shard_step_timing(ctx, plan, payload, pts, param, out, flags, reps, warm=2):
 
 
 def two_plan_timing(ctx, m, n, launch, payload, pts, param, flags, reps):
-    """N = 1 only: the same step on two plans (two scratch sets and outputs), launched
-    alternately on two streams, so that step k+1's first kernels overlap step k's
-    last ones (the usage for a stream of batches); mean ms per step over `reps`
-    steps between two events, and the records of the last two steps."""
+    """The same (sharded) step on two plans (two scratch sets, outputs and records),
+    launched alternately on two streams, so that step k+1's first kernels overlap step
+    k's last ones (the usage for a stream of batches).  At N > 1 each step's record is
+    all-gathered and combined on the step's own stream (ProcessGroupNCCL runs the
+    collectives on its internal stream, in call order on every rank).  Mean ms per
+    step over `reps` steps between two events, max over ranks, and the combined
+    records of the last two steps."""
     torch, sm = ctx.torch, ctx.sm
     s0, s1 = ctx.stream, torch.cuda.Stream(device=ctx.dev)
     gs = []
     for _ in range(2):
-        plan = sm.smap_plan(m, n, device=ctx.local, **launch)
+        plan = sm.smap_plan(m, n, shard_rank=ctx.rank, shard_count=ctx.G, device=ctx.local, **launch)
         out = sm.alloc_out(plan, payload, device=ctx.dev)
         rec = torch.zeros(7, dtype=torch.int64, device=ctx.dev)
+        gat = torch.zeros(ctx.G * 7, dtype=torch.int64, device=ctx.dev)
         gs.append((plan, out, rec, sm.smap_graph_capture(plan, payload, points=pts, param=param, out=out,
-                                                         flags=flags, record=rec)))
+                                                         flags=flags, record=rec), gat))
+
+    def step(i):
+        st = s0 if i % 2 == 0 else s1
+        g = gs[i % 2]
+        with torch.cuda.stream(st):
+            sm.smap_graph_launch(g[3], stream=st)
+            if ctx.G > 1:
+                ctx.dist.all_gather_into_tensor(g[4], g[2])
+                sm.smap_result_combine(g[4], ctx.G, g[2], stream=st)
 
     def run(k):
         e0, e1 = ctx.event(), ctx.event()
+        ctx.barrier()
         e0.record(s0)
         s1.wait_event(e0)
         for i in range(k):
-            sm.smap_graph_launch(gs[i % 2][3], stream=s0 if i % 2 == 0 else s1)
-        j = ctx.torch.cuda.Event()
+            step(i)
+        j = torch.cuda.Event()
         j.record(s1)
         s0.wait_event(j)
         e1.record(s0)
-        torch.cuda.synchronize()
+        ctx.barrier()
         return e0.elapsed_time(e1) / max(k, 1)
 
     run(4)
-    ms = run(reps)
+    (ms,) = ctx.max_over_ranks(run(reps))
     recs = [sm.result_dict(g[2]) for g in gs]
     del gs
     return ms, recs
@@ -401,7 +415,7 @@ def sharded_configs(ctx, golden):
              "checked_vs_oracle": bool(ok)}
         if payload == "index_write":
             e["achieved_gbs_kernel"] = round(V * 8 / ctx.G / (kern_max * 1e-3) / 1e9, 1)
-        if ctx.G == 1 and name != "C4":
+        if name != "C4":
             # two steps in flight (two plans, two streams): every step's record checked
             tms, recs = two_plan_timing(ctx, m, n, launch, payload, pts, param, flags, 2 * reps)
             tok = all(r["count"] == V for r in recs)
@@ -413,9 +427,10 @@ def sharded_configs(ctx, golden):
                 tok = tok and all(abs(r["sum"] - g["atm_sum"]) <= 1e-5 * abs(g["atm_sum"]) for r in recs)
             e["two_plans"] = {"ms_per_step": round(tms, 4), "elements_per_s": V / (tms * 1e-3),
                               "checked_vs_oracle": bool(tok),
-                              "what": "N = 1: the step on two plans (two pair bitmaps / result blocks / outputs) "
-                                      "alternating over two streams, steps back to back: a step's pre-pass and "
-                                      "first tiles overlap the previous step's tail (a stream of batches)"}
+                              "what": "the step (incl. the record all-gather + combine at N > 1) on two plans "
+                                      "(two pair bitmaps / result blocks / outputs) alternating over two streams, "
+                                      "steps back to back, max over ranks: a step's pre-pass and first tiles "
+                                      "overlap the previous step's tail (a stream of batches)"}
         if name == "C5X":
             e["note"] = "supplementary scaling workload (n=8192, 64x the triples of C5), not a BASELINE config"
         res[name] = e

@@ -34,3 +34,5 @@ def test_bench_two_ranks_on_one_gpu():
     assert d["checksum"]["count"] == d["checksum"]["expected_count"]
     for name, e in d["configs_sharded"].items():
         assert e["checked_vs_oracle"] is True, name
+        if name != "C4":                                        # two plans in flight, records combined per step
+            assert e["two_plans"]["checked_vs_oracle"] is True, name
