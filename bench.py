@@ -26,7 +26,8 @@ Besides the headline line the same JSON object carries (DESIGN.md s.10):
                    ATM), C4 (u64 index write, 68.7 GB) and C5 (triple correlation),
                    plus the supplementary C5 at n = 8192, each rank running its
                    omega_x shard, the step = kernel + record + all-gather + combine,
-                   max over ranks, checked against the oracle's values
+                   max over ranks, checked against the oracle's values; for the
+                   m = 3 jobs also with two plans in flight (`two_plans`)
   configs          (N = 1) lambda vs BB per config at the product and at the paper's
                    launch, wasted-thread fractions against the closed forms, the
                    EMPTY-block (K10) cap, FP32-pipe / issue fractions, the targets
