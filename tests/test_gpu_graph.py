@@ -126,3 +126,41 @@ def test_record_buffers_checked_by_the_binding(sm):
     with pytest.raises(ValueError):
         sm.smap_result_combine(torch.zeros(7, dtype=torch.int64, device="cuda"), 2,
                                torch.zeros(7, dtype=torch.int64, device="cuda"))   # 2 records need 112 bytes
+
+
+@pytest.mark.parametrize("m,n,kw,payload,param,flags_name,P", [
+    (3, 1024, dict(rho=64, granularity="tile", persistent=32), "tc", 0.5, "none", 3),
+    (3, 512, dict(rho=32, granularity="tile", layout="tiles"), "index_write_atm", 1e-2, "xor", 2),
+    (3, 1024, dict(rho=64, granularity="tile", persistent=16, shard_rank=1, shard_count=4), "tc", 0.5, "none", 2),
+])
+def test_plans_in_flight_round_robin(sm, orc, m, n, kw, payload, param, flags_name, P):
+    """Several steps in flight (`two_plans`): P plans of the same
+    (shard of the) workload, their captured steps launched round robin on P streams
+    with no ordering between consecutive steps; every plan's record equals the one
+    of a plain smap_run, bit for bit (each plan owns its scratch, output and result
+    block, so concurrent steps cannot interfere)."""
+    flags = sm.RUN_XOR if flags_name == "xor" else 0
+    p = workloads.points(n, 13)
+    pts = torch.from_numpy(p).cuda()
+    ref_plan = sm.smap_plan(m, n, **kw)
+    ref_out = sm.alloc_out(ref_plan, payload)
+    sm.smap_run(ref_plan, payload, points=pts, param=param, out=ref_out, flags=flags)
+    ref = torch.zeros(7, dtype=torch.int64, device="cuda")
+    sm.smap_result_reduce(ref_plan, ref)
+    want = sm.result_dict(ref)
+    streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(P - 1)]
+    gs = []
+    for _ in range(P):
+        plan = sm.smap_plan(m, n, **kw)
+        out = sm.alloc_out(plan, payload)
+        rec = torch.zeros(7, dtype=torch.int64, device="cuda")
+        gs.append((plan, out, rec, sm.smap_graph_capture(plan, payload, points=pts, param=param, out=out,
+                                                         flags=flags, record=rec)))
+    torch.cuda.synchronize()
+    for k in range(4 * P + 1):
+        sm.smap_graph_launch(gs[k % P][3], stream=streams[k % P])
+    torch.cuda.synchronize()
+    for g in gs:
+        assert sm.result_dict(g[2]) == want
+    if payload == "tc" and "shard_count" not in kw:
+        assert want["tc"] == orc.tc_count(p, np.float32(param))
